@@ -1,0 +1,126 @@
+/*
+ * tsketch.h -- C ABI of libtsketch, the B200 (sm_100a) hot path of the tensor-based
+ * sketching method for low-rank approximation of matrix streams (arXiv 2209.14637).
+ *
+ * Problem (Eq. (1)): for every matrix A_d (m x n) of a stream,
+ *     min_B ||A_d - B||_F  s.t.  rank(B) <= r.
+ * Method (Algorithm 2):
+ *   1. tensorise the training matrices A_1..A_D' (m x n) into a third-order tensor;
+ *   2. S <- Tucker1 of that tensor along mode 1, i.e. S* = (U^(1))_k^T, the first k
+ *      left singular vectors of A_(1) = [A_1|...|A_D'] -- computed here as the
+ *      top-k eigenvectors of the mode-1 Gram G = A_(1) A_(1)^T = sum_d A_d A_d^T;
+ *   3. A_hat <- SCW(A, S, r) for every test matrix A (Algorithm 1).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - Matrices are fp32 (inputs/outputs named float*) or fp64 (double*), ROW-MAJOR and
+ *   contiguous.  A stack of matrices [B][m][n] is slice-major (matrix b starts at b*m*n).
+ * - Pointers may be DEVICE pointers (current device of the ctx) or HOST pointers (pageable or
+ *   pinned).  The library detects which with cudaPointerGetAttributes: host inputs are copied
+ *   to device workspace and host outputs are copied back before the call returns (the call is
+ *   then synchronous).  With device pointers every call is asynchronous on the ctx stream.
+ * - Alignment: device pointers to fp32 matrices must be 16-byte aligned and n % 4 == 0
+ *   (TMA row pitch), else TSK_ESHAPE.
+ * - Ownership: the caller owns all buffers; the library never frees or retains them past
+ *   the call's stream completion.  The ctx owns its workspace.
+ * - Errors: argument errors return synchronously and enqueue nothing.  Device faults surface
+ *   as TSK_ECUDA on this or a later call (or tsk_sync).
+ * - Threading: one ctx per host thread/stream; different ctxs are independent.
+ * - Determinism: fixed reduction orders, no floating-point atomics: identical inputs give
+ *   bit-identical outputs.
+ */
+#ifndef TSKETCH_H_
+#define TSKETCH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsk_ctx_s* tsk_ctx;
+
+typedef enum {
+  TSK_OK = 0,
+  TSK_WARN_RANK_CLAMPED = 1,  /* r > k: r clamped to k (reading c7); results valid */
+  TSK_WARN_NOT_CONVERGED = 2, /* eigensolver hit max_iters; S valid but not converged */
+  TSK_EINVAL = -1,            /* bad scalar: k < 1, k > m, r < 1, D < 1, B < 0, m/n < 1 */
+  TSK_ESHAPE = -2,            /* n % 4 != 0, misaligned pointer */
+  TSK_ENOMEM = -3,            /* device workspace allocation failed */
+  TSK_ECUDA = -4,             /* CUDA runtime / launch / device fault */
+  TSK_EDEVICE = -6,           /* device is not compute capability 10.0 (sm_100a) */
+  TSK_ENULL = -8              /* a required pointer is NULL */
+} tsk_status;
+
+/* Create a context on `device`, enqueueing on `cuda_stream` (a cudaStream_t; NULL = legacy
+   default stream).  Fails with TSK_EDEVICE unless the device is sm_100. */
+tsk_status tsk_create(tsk_ctx* out, int device, void* cuda_stream);
+tsk_status tsk_destroy(tsk_ctx ctx);
+/* Re-target subsequent work to another stream of the same device. */
+tsk_status tsk_set_stream(tsk_ctx ctx, void* cuda_stream);
+/* Block until all work enqueued by this ctx has completed; reports deferred device faults. */
+tsk_status tsk_sync(tsk_ctx ctx);
+const char* tsk_status_string(tsk_status s);
+/* Number of kernels this ctx has launched since creation (bench evidence). */
+int64_t tsk_launch_count(tsk_ctx ctx);
+
+/* ---------------------------------------------------------------------- training */
+
+typedef struct {
+  int oversample;    /* block size p = min(m, k + oversample); default (<= 0): k + max(k, 16) */
+  int max_iters;     /* subspace iterations cap; default 300 */
+  double tol;        /* convergence: Ritz residual <= tol * theta_1 for the top k; default 1e-6 */
+  int dense_max_m;   /* m <= this: one dense Jacobi eigensolve of G; default 256 */
+  int gemm_chain;    /* tuning: K-chunks per TMEM accumulation chain (0 = default) */
+  int gemm_splits;   /* tuning: K splits of the Gram (0 = auto) */
+} tsk_train_opts;
+
+typedef struct {
+  int iters;          /* subspace iterations run (0 for the dense path) */
+  double kyfan;       /* sum_{i<k} theta_i, the Ky Fan energy tr(S G S^T) */
+  double max_resid;   /* max_{i<k} ||G s_i - theta_i s_i|| / theta_1 */
+  int gram_splits;    /* K splits used by the Gram kernel */
+  int gram_tiles;     /* 128x128 output tiles computed (lower triangle) */
+} tsk_train_info;
+
+/* Mode-1 Gram of a stack of D training matrices:
+     G (+)= sum_{d<D} A_d A_d^T          A: [D][m][n] fp32;  G64: [m][m] fp64 (required)
+   G32 (optional, may be NULL): fp32 copy of the result.  accumulate != 0 adds into G64
+   (streaming: call once per chunk of the stream).  Only the lower-triangle 128x128 tiles are
+   computed (3xTF32 tensor cores) and mirrored, so G64 is exactly symmetric. */
+tsk_status sketch_gram(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, float* G32,
+                       int accumulate, const tsk_train_opts* opts, tsk_train_info* info);
+
+/* Top-k eigenvectors of the symmetric PSD Gram: S [k][m] fp32 with orthonormal
+   rows ordered by decreasing eigenvalue, each row sign-normalised (largest-|entry| positive,
+   reading c5); lambda [k] fp64 (may be NULL) the Ritz values.  G64 [m][m] fp64. */
+tsk_status sketch_topk(tsk_ctx ctx, const double* G64, int m, int k, float* S, double* lambda,
+                       const tsk_train_opts* opts, tsk_train_info* info);
+
+/* Algorithm 2 lines 1-2 on one GPU: sketch_gram followed by sketch_topk.  G64_out (optional)
+   receives the Gram.  Multi-GPU: call sketch_gram on each rank's contiguous shard, all-reduce G64
+   (sum), then sketch_topk on every rank (deterministic, identical S everywhere). */
+tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S, double* lambda,
+                        double* G64_out, const tsk_train_opts* opts, tsk_train_info* info);
+
+/* ---------------------------------------------------------------------- test stream */
+
+/* SCW (Algorithm 1) on a batch of B test matrices A [B][m][n] with the sketch
+   S [k][m]:  V = orthonormal basis of rowspace(S A_b) (QR/eigen orthonormalisation),
+   [A_b V]_r by the SVD of A_b V, A_hat_b = [A_b V]_r V^T = L_b R_b^T with
+     L [B][m][r] = U_r diag(sigma_r),   R [B][n][r] = V W_r (orthonormal columns),
+     sigma [B][r] fp32 the singular values of A_b V (decreasing).
+   Any of L, R, sigma may be NULL.  r > k is clamped to k (TSK_WARN_RANK_CLAMPED); r <= min(m,n). */
+tsk_status sketch_apply_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
+                            float* L, float* R, float* sigma);
+
+/* Per-matrix SCW error err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64, dense residual with an fp64
+   reduction, not ||A||^2 - sum sigma^2).  err: [B] fp64 (device or host). */
+tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
+                     double* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSKETCH_H_ */

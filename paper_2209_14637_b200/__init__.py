@@ -1,0 +1,264 @@
+"""paper_2209_14637_b200 -- B200-native hot path of the tensor-based sketch (arXiv 2209.14637).
+
+Thin Python binding of ``libtsketch.so`` (the C ABI declared in ``include/tsketch.h``).
+The functions here carry the same names as the C entry points and only marshal arguments:
+every step of the path (Gram, eigensolver, SCW, errors) runs in the library's CUDA kernels.
+There is no CPU fallback: importing works without a GPU (so symbol checks can run on CPU),
+but every compute call requires the built library and a B200 and raises otherwise.
+
+Tensors may live on the GPU (device pointers, asynchronous on the current torch stream) or
+on the CPU (host pointers: the library stages them through device memory and copies results
+back, synchronously -- the end-to-end path).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import warnings
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsketch.so")
+
+TSK_OK = 0
+TSK_WARN_RANK_CLAMPED = 1
+TSK_WARN_NOT_CONVERGED = 2
+STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVERGED", -1: "TSK_EINVAL",
+                -2: "TSK_ESHAPE", -3: "TSK_ENOMEM", -4: "TSK_ECUDA", -6: "TSK_EDEVICE", -8: "TSK_ENULL"}
+
+# every symbol include/tsketch.h declares (checked by tests/test_abi.py on CPU)
+EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_status_string", "tsk_launch_count",
+            "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error"]
+
+
+class TskError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {STATUS_NAMES.get(status, status)} ({_status_string(status)})")
+
+
+class TrainOpts(ctypes.Structure):
+    _fields_ = [("oversample", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
+                ("dense_max_m", ctypes.c_int), ("gemm_chain", ctypes.c_int), ("gemm_splits", ctypes.c_int)]
+
+
+class TrainInfo(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("kyfan", ctypes.c_double), ("max_resid", ctypes.c_double),
+                ("gram_splits", ctypes.c_int), ("gram_tiles", ctypes.c_int)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libtsketch.so (built in-tree by ``python paper_2209_14637_b200/build.py``)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libtsketch.so not built ({LIB_PATH}); run __graft_entry__.build() -- "
+                               "there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, f32p, f64p = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p
+        L.tsk_create.argtypes = [ctypes.POINTER(vp), i32, vp]
+        L.tsk_destroy.argtypes = [vp]
+        L.tsk_set_stream.argtypes = [vp, vp]
+        L.tsk_sync.argtypes = [vp]
+        L.tsk_status_string.argtypes = [i32]
+        L.tsk_status_string.restype = ctypes.c_char_p
+        L.tsk_launch_count.argtypes = [vp]
+        L.tsk_launch_count.restype = i64
+        L.sketch_gram.argtypes = [vp, f32p, i64, i32, i32, f64p, f32p, i32, vp, vp]
+        L.sketch_topk.argtypes = [vp, f64p, i32, i32, f32p, f64p, vp, vp]
+        L.sketch_train.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, f64p, vp, vp]
+        L.sketch_apply_scw.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, i32, f32p, f32p, f32p]
+        L.scw_error.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, i32, f64p]
+        for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
+                  "sketch_train", "sketch_apply_scw", "scw_error"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def _status_string(s: int) -> str:
+    try:
+        return lib().tsk_status_string(s).decode()
+    except Exception:  # library missing
+        return "?"
+
+
+def _check(status: int, what: str) -> int:
+    if status < 0:
+        raise TskError(status, what)
+    if status == TSK_WARN_NOT_CONVERGED:
+        warnings.warn(f"{what}: eigensolver reached max_iters (S valid, not converged)", RuntimeWarning)
+    elif status == TSK_WARN_RANK_CLAMPED:
+        warnings.warn(f"{what}: r > k, clamped to k", RuntimeWarning)
+    return status
+
+
+class Context:
+    """A libtsketch context (tsk_ctx) on one CUDA device; follows torch's current stream."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2209_14637_b200 needs a CUDA (sm_100a) device; no CPU fallback")
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            _check(lib().tsk_create(ctypes.byref(h), self.device.index, ctypes.c_void_p(stream)), "tsk_create")
+        self.handle = h
+
+    def _bind_stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _check(lib().tsk_set_stream(self.handle, ctypes.c_void_p(s)), "tsk_set_stream")
+
+    def sync(self):
+        _check(lib().tsk_sync(self.handle), "tsk_sync")
+
+    @property
+    def launches(self) -> int:
+        return int(lib().tsk_launch_count(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().tsk_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_ctx_cache: dict = {}
+
+
+def context(device=None) -> Context:
+    if device is None:
+        device = torch.cuda.current_device()
+    key = torch.device("cuda", device).index if isinstance(device, int) else torch.device(device).index
+    if key not in _ctx_cache:
+        _ctx_cache[key] = Context(key)
+    ctx = _ctx_cache[key]
+    ctx._bind_stream()
+    return ctx
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _need(t: torch.Tensor, dtype, name: str, ndim: int):
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or t.dim() != ndim or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor with {ndim} dims")
+
+
+def _alloc(shape, dtype, like: torch.Tensor):
+    if like.is_cuda:
+        return torch.empty(shape, dtype=dtype, device=like.device)
+    return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+
+def _opts(opts) -> Optional[TrainOpts]:
+    if opts is None:
+        return None
+    if isinstance(opts, TrainOpts):
+        return opts
+    o = TrainOpts()
+    for k, v in dict(opts).items():
+        setattr(o, k, v)
+    return o
+
+
+def _optref(o):
+    return ctypes.byref(o) if o is not None else None
+
+
+# ------------------------------------------------------------------------------------ C-ABI names
+def sketch_gram(A: torch.Tensor, G64: Optional[torch.Tensor] = None, G32: Optional[torch.Tensor] = None,
+                accumulate: bool = False, opts=None, ctx: Optional[Context] = None):
+    """G64 (+)= sum_d A_d A_d^T for A [D, m, n] fp32.  Returns (G64, info)."""
+    _need(A, torch.float32, "A", 3)
+    D, m, n = A.shape
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    if G64 is None:
+        if accumulate:
+            raise ValueError("accumulate requires G64")
+        G64 = _alloc((m, m), torch.float64, A)
+    _need(G64, torch.float64, "G64", 2)
+    info = TrainInfo()
+    o = _opts(opts)
+    _check(lib().sketch_gram(ctx.handle, _ptr(A), D, m, n, _ptr(G64), _ptr(G32), int(bool(accumulate)), _optref(o),
+                             ctypes.byref(info)), "sketch_gram")
+    return G64, info
+
+
+def sketch_topk(G64: torch.Tensor, k: int, opts=None, ctx: Optional[Context] = None):
+    """Top-k eigenvectors of G as rows of S [k, m] fp32 and Ritz values lambda [k] fp64."""
+    _need(G64, torch.float64, "G64", 2)
+    m = G64.shape[0]
+    ctx = ctx or context(G64.device if G64.is_cuda else None)
+    S = _alloc((k, m), torch.float32, G64)
+    lam = _alloc((k,), torch.float64, G64)
+    info = TrainInfo()
+    o = _opts(opts)
+    st = _check(lib().sketch_topk(ctx.handle, _ptr(G64), m, k, _ptr(S), _ptr(lam), _optref(o), ctypes.byref(info)),
+                "sketch_topk")
+    return S, lam, info, st
+
+
+def sketch_train(A: torch.Tensor, k: int, opts=None, G64_out: Optional[torch.Tensor] = None,
+                 ctx: Optional[Context] = None):
+    """Algorithm 2 lines 1-2 on one GPU.  Returns (S, lambda, info, status)."""
+    _need(A, torch.float32, "A", 3)
+    D, m, n = A.shape
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    S = _alloc((k, m), torch.float32, A)
+    lam = _alloc((k,), torch.float64, A)
+    info = TrainInfo()
+    o = _opts(opts)
+    st = _check(lib().sketch_train(ctx.handle, _ptr(A), D, m, n, k, _ptr(S), _ptr(lam), _ptr(G64_out), _optref(o),
+                                   ctypes.byref(info)), "sketch_train")
+    return S, lam, info, st
+
+
+def sketch_apply_scw(A: torch.Tensor, S: torch.Tensor, r: int, want=("L", "R", "sigma"),
+                     ctx: Optional[Context] = None):
+    """SCW (Algorithm 1) on a batch A [B, m, n]: A_hat_b = L_b R_b^T."""
+    _need(A, torch.float32, "A", 3)
+    _need(S, torch.float32, "S", 2)
+    B, m, n = A.shape
+    k = S.shape[0]
+    rr = min(r, k)
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    L = _alloc((B, m, rr), torch.float32, A) if "L" in want else None
+    R = _alloc((B, n, rr), torch.float32, A) if "R" in want else None
+    sig = _alloc((B, rr), torch.float32, A) if "sigma" in want else None
+    _check(lib().sketch_apply_scw(ctx.handle, _ptr(A), B, m, n, _ptr(S), k, r, _ptr(L), _ptr(R), _ptr(sig)),
+           "sketch_apply_scw")
+    return L, R, sig
+
+
+def scw_error(A: torch.Tensor, S: torch.Tensor, r: int, out: Optional[torch.Tensor] = None,
+              ctx: Optional[Context] = None) -> torch.Tensor:
+    """err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64, dense residual)."""
+    _need(A, torch.float32, "A", 3)
+    _need(S, torch.float32, "S", 2)
+    B, m, n = A.shape
+    k = S.shape[0]
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    err = out if out is not None else _alloc((B,), torch.float64, A)
+    _check(lib().scw_error(ctx.handle, _ptr(A), B, m, n, _ptr(S), k, r, _ptr(err)), "scw_error")
+    return err
+
+
+from .dist import shard_range, train  # noqa: E402,F401

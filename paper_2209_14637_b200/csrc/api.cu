@@ -1,0 +1,432 @@
+// C-ABI entry points of libtsketch (include/tsketch.h): argument validation, host/device
+// pointer handling, and composition of the kernels into the calls of Algorithm 2
+// (PAPER.md:156-169).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "tsk_internal.h"
+
+using tsk::Ctx;
+
+namespace {
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+tsk_status cuda_ok(cudaError_t e) {
+  if (e == cudaSuccess) return TSK_OK;
+  cudaGetLastError();
+  return e == cudaErrorMemoryAllocation ? TSK_ENOMEM : TSK_ECUDA;
+}
+
+bool is_error(tsk_status s) { return (int)s < 0; }
+
+// Device view of a possibly-host buffer: allocated from a dedicated ctx workspace slot.
+struct DevBuf {
+  void* dev = nullptr;
+  const void* user = nullptr;
+  size_t bytes = 0;
+  bool staged = false;
+};
+
+tsk_status stage_out(Ctx* c, DevBuf& b) {
+  if (!b.staged || !b.user) return TSK_OK;
+  tsk_status s = cuda_ok(cudaMemcpyAsync(const_cast<void*>(b.user), b.dev, b.bytes, cudaMemcpyDeviceToHost, c->stream));
+  if (is_error(s)) return s;
+  return cuda_ok(cudaStreamSynchronize(c->stream));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- extended ctx (streams for e2e)
+struct CtxExt {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t copied[2] = {nullptr, nullptr};
+  cudaEvent_t consumed[2] = {nullptr, nullptr};
+  void* buf[2] = {nullptr, nullptr};
+  size_t buf_bytes = 0;
+  void* dev_small[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t dev_small_bytes[4] = {0, 0, 0, 0};
+};
+
+struct tsk_ctx_full {
+  tsk_ctx_s base;
+  CtxExt ext;
+};
+
+static CtxExt* ext_of(tsk_ctx ctx) { return &reinterpret_cast<tsk_ctx_full*>(ctx)->ext; }
+
+static void* small_ws(tsk_ctx ctx, int slot, size_t bytes) {
+  CtxExt* e = ext_of(ctx);
+  if (e->dev_small_bytes[slot] >= bytes) return e->dev_small[slot];
+  if (e->dev_small[slot]) {
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaFree(e->dev_small[slot]);
+  }
+  e->dev_small[slot] = nullptr;
+  e->dev_small_bytes[slot] = 0;
+  if (cudaMalloc(&e->dev_small[slot], bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  e->dev_small_bytes[slot] = bytes;
+  return e->dev_small[slot];
+}
+
+// stage through an ext slot (used for outputs / small inputs)
+static tsk_status stage_slot(tsk_ctx ctx, const void* user, size_t bytes, int slot, DevBuf& out, bool copy_in) {
+  out.user = user;
+  out.bytes = bytes;
+  if (is_device_ptr(user)) {
+    out.dev = const_cast<void*>(user);
+    out.staged = false;
+    return TSK_OK;
+  }
+  out.dev = small_ws(ctx, slot, bytes);
+  if (!out.dev) return TSK_ENOMEM;
+  out.staged = true;
+  if (copy_in) return cuda_ok(cudaMemcpyAsync(out.dev, user, bytes, cudaMemcpyHostToDevice, ctx->c.stream));
+  return TSK_OK;
+}
+
+extern "C" {
+
+const char* tsk_status_string(tsk_status s) {
+  switch (s) {
+    case TSK_OK: return "ok";
+    case TSK_WARN_RANK_CLAMPED: return "warning: r clamped to k";
+    case TSK_WARN_NOT_CONVERGED: return "warning: eigensolver reached max_iters";
+    case TSK_EINVAL: return "invalid argument";
+    case TSK_ESHAPE: return "unsupported shape / alignment (n % 4 != 0 or misaligned pointer)";
+    case TSK_ENOMEM: return "device allocation failed";
+    case TSK_ECUDA: return "CUDA error";
+    case TSK_EDEVICE: return "device is not sm_100 (B200)";
+    case TSK_ENULL: return "required pointer is NULL";
+  }
+  return "unknown status";
+}
+
+tsk_status tsk_create(tsk_ctx* out, int device, void* cuda_stream) {
+  if (!out) return TSK_ENULL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return TSK_EDEVICE;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return TSK_ECUDA;
+  if (prop.major != 10 || prop.minor != 0) return TSK_EDEVICE;
+  if (cudaSetDevice(device) != cudaSuccess) return TSK_ECUDA;
+  auto* full = new (std::nothrow) tsk_ctx_full();
+  if (!full) return TSK_ENOMEM;
+  full->base.c.device = device;
+  full->base.c.num_sms = prop.multiProcessorCount;
+  full->base.c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  *out = &full->base;
+  return TSK_OK;
+}
+
+tsk_status tsk_destroy(tsk_ctx ctx) {
+  if (!ctx) return TSK_ENULL;
+  Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.stream);
+  for (int i = 0; i < tsk::WS_COUNT; ++i)
+    if (c.ws[i]) cudaFree(c.ws[i]);
+  if (c.host_pinned) cudaFreeHost(c.host_pinned);
+  CtxExt* e = ext_of(ctx);
+  for (int i = 0; i < 2; ++i) {
+    if (e->buf[i]) cudaFree(e->buf[i]);
+    if (e->copied[i]) cudaEventDestroy(e->copied[i]);
+    if (e->consumed[i]) cudaEventDestroy(e->consumed[i]);
+  }
+  for (int i = 0; i < 4; ++i)
+    if (e->dev_small[i]) cudaFree(e->dev_small[i]);
+  if (e->copy) cudaStreamDestroy(e->copy);
+  delete reinterpret_cast<tsk_ctx_full*>(ctx);
+  return TSK_OK;
+}
+
+tsk_status tsk_set_stream(tsk_ctx ctx, void* cuda_stream) {
+  if (!ctx) return TSK_ENULL;
+  ctx->c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return TSK_OK;
+}
+
+tsk_status tsk_sync(tsk_ctx ctx) {
+  if (!ctx) return TSK_ENULL;
+  return cuda_ok(cudaStreamSynchronize(ctx->c.stream));
+}
+
+int64_t tsk_launch_count(tsk_ctx ctx) { return ctx ? ctx->c.launches : -1; }
+
+// ------------------------------------------------------------------------------ training
+static tsk_status gram_device(Ctx* c, const float* A, int64_t D, int m, int n, double* G64, float* G32,
+                              int accumulate, const tsk_train_opts* opts, tsk_train_info* info) {
+  tsk::GemmProblem p;
+  p.X = A;
+  p.Y = A;
+  p.M = m;
+  p.N = m;
+  p.n = n;
+  p.D = D;
+  p.x_row_stride = n;
+  p.x_slice_stride = (long long)m * n;
+  p.y_row_stride = n;
+  p.y_slice_stride = (long long)m * n;
+  p.sym = 1;
+  p.out64 = G64;
+  p.ldo64 = m;
+  p.out32 = G32;
+  p.ldo32 = m;
+  p.accumulate = accumulate;
+  if (opts) {
+    p.chain = opts->gemm_chain;
+    p.splits = opts->gemm_splits;
+  }
+  tsk::GemmInfo gi;
+  p.info = &gi;
+  tsk_status s = tsk::gemm_tf32x3(c, p);
+  if (info && s == TSK_OK) {
+    info->gram_splits = gi.splits;
+    info->gram_tiles = gi.tiles;
+  }
+  return s;
+}
+
+// Host-resident training stack: stream it through two device buffers, overlapping the
+// H2D copy of chunk i+1 with the Gram of chunk i (accumulating into G64).
+static tsk_status gram_host(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, float* G32,
+                            int accumulate, const tsk_train_opts* opts, tsk_train_info* info) {
+  Ctx* c = &ctx->c;
+  CtxExt* e = ext_of(ctx);
+  const size_t mat = (size_t)m * n * 4;
+  const size_t target = (size_t)256 << 20;  // 256 MiB per staging buffer
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(target / mat));
+  chunk = std::min<int64_t>(chunk, D);
+  const size_t bytes = (size_t)chunk * mat;
+  if (!e->copy) {
+    if (cudaStreamCreateWithFlags(&e->copy, cudaStreamNonBlocking) != cudaSuccess) return TSK_ECUDA;
+    for (int i = 0; i < 2; ++i) {
+      cudaEventCreateWithFlags(&e->copied[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&e->consumed[i], cudaEventDisableTiming);
+    }
+  }
+  if (e->buf_bytes < bytes) {
+    cudaStreamSynchronize(c->stream);
+    for (int i = 0; i < 2; ++i) {
+      if (e->buf[i]) cudaFree(e->buf[i]);
+      e->buf[i] = nullptr;
+      if (cudaMalloc(&e->buf[i], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        e->buf_bytes = 0;
+        return TSK_ENOMEM;
+      }
+    }
+    e->buf_bytes = bytes;
+  }
+  // the copy stream must not start before earlier work on the compute stream released the buffers
+  cudaEventRecord(e->consumed[0], c->stream);
+  cudaEventRecord(e->consumed[1], c->stream);
+  int i = 0;
+  for (int64_t d0 = 0; d0 < D; d0 += chunk, i ^= 1) {
+    const int64_t dc = std::min<int64_t>(chunk, D - d0);
+    cudaStreamWaitEvent(e->copy, e->consumed[i], 0);
+    if (cudaMemcpyAsync(e->buf[i], A + (size_t)d0 * m * n, (size_t)dc * mat, cudaMemcpyHostToDevice, e->copy) !=
+        cudaSuccess)
+      return TSK_ECUDA;
+    cudaEventRecord(e->copied[i], e->copy);
+    cudaStreamWaitEvent(c->stream, e->copied[i], 0);
+    const bool last = d0 + dc >= D;
+    tsk_status s = gram_device(c, reinterpret_cast<const float*>(e->buf[i]), dc, m, n, G64, last ? G32 : nullptr,
+                               (d0 == 0) ? accumulate : 1, opts, info);
+    if (is_error(s)) return s;
+    cudaEventRecord(e->consumed[i], c->stream);
+  }
+  return TSK_OK;
+}
+
+tsk_status sketch_gram(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, float* G32, int accumulate,
+                       const tsk_train_opts* opts, tsk_train_info* info) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !G64) return TSK_ENULL;
+  if (D < 1 || m < 1 || n < 1) return TSK_EINVAL;
+  if (n % 4) return TSK_ESHAPE;
+  Ctx* c = &ctx->c;
+  cudaSetDevice(c->device);
+  DevBuf g64, g32;
+  tsk_status s = stage_slot(ctx, G64, (size_t)m * m * 8, 0, g64, accumulate != 0);
+  if (is_error(s)) return s;
+  if (G32) {
+    s = stage_slot(ctx, G32, (size_t)m * m * 4, 1, g32, false);
+    if (is_error(s)) return s;
+  }
+  float* g32d = G32 ? reinterpret_cast<float*>(g32.dev) : nullptr;
+  if (is_device_ptr(A))
+    s = gram_device(c, A, D, m, n, reinterpret_cast<double*>(g64.dev), g32d, accumulate, opts, info);
+  else
+    s = gram_host(ctx, A, D, m, n, reinterpret_cast<double*>(g64.dev), g32d, accumulate, opts, info);
+  if (is_error(s)) return s;
+  if (g64.staged) {
+    if (is_error(s = stage_out(&ctx->c, g64))) return s;
+  }
+  if (G32 && g32.staged) {
+    if (is_error(s = stage_out(&ctx->c, g32))) return s;
+  }
+  return TSK_OK;
+}
+
+tsk_status sketch_topk(tsk_ctx ctx, const double* G64, int m, int k, float* S, double* lambda,
+                       const tsk_train_opts* opts, tsk_train_info* info) {
+  if (!ctx) return TSK_ENULL;
+  if (!G64 || !S) return TSK_ENULL;
+  if (m < 1 || k < 1 || k > m) return TSK_EINVAL;
+  if (m > 256 && k > 192) return TSK_EINVAL;
+  cudaSetDevice(ctx->c.device);
+  DevBuf g, sb, lb;
+  tsk_status s = stage_slot(ctx, G64, (size_t)m * m * 8, 0, g, true);
+  if (is_error(s)) return s;
+  if (is_error(s = stage_slot(ctx, S, (size_t)k * m * 4, 2, sb, false))) return s;
+  if (lambda && is_error(s = stage_slot(ctx, lambda, (size_t)k * 8, 3, lb, false))) return s;
+  tsk_status r = tsk::topk_eigen(&ctx->c, reinterpret_cast<const double*>(g.dev), m, k,
+                                 reinterpret_cast<float*>(sb.dev), lambda ? reinterpret_cast<double*>(lb.dev) : nullptr,
+                                 opts, info);
+  if (is_error(r)) return r;
+  if (is_error(s = stage_out(&ctx->c, sb))) return s;
+  if (lambda && is_error(s = stage_out(&ctx->c, lb))) return s;
+  return r;
+}
+
+tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S, double* lambda,
+                        double* G64_out, const tsk_train_opts* opts, tsk_train_info* info) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !S) return TSK_ENULL;
+  if (D < 1 || m < 1 || n < 1 || k < 1 || k > m) return TSK_EINVAL;
+  if (m > 256 && k > 192) return TSK_EINVAL;
+  if (n % 4) return TSK_ESHAPE;
+  Ctx* c = &ctx->c;
+  cudaSetDevice(c->device);
+  double* G = nullptr;
+  const bool g_dev = G64_out && is_device_ptr(G64_out);
+  if (g_dev) {
+    G = G64_out;
+  } else {
+    G = reinterpret_cast<double*>(c->workspace(tsk::WS_GRAM, (size_t)m * m * 8));
+    if (!G) return TSK_ENOMEM;
+  }
+  tsk_status s;
+  if (is_device_ptr(A))
+    s = gram_device(c, A, D, m, n, G, nullptr, 0, opts, info);
+  else
+    s = gram_host(ctx, A, D, m, n, G, nullptr, 0, opts, info);
+  if (is_error(s)) return s;
+  DevBuf sb, lb;
+  if (is_error(s = stage_slot(ctx, S, (size_t)k * m * 4, 2, sb, false))) return s;
+  if (lambda && is_error(s = stage_slot(ctx, lambda, (size_t)k * 8, 3, lb, false))) return s;
+  tsk_status r = tsk::topk_eigen(c, G, m, k, reinterpret_cast<float*>(sb.dev),
+                                 lambda ? reinterpret_cast<double*>(lb.dev) : nullptr, opts, info);
+  if (is_error(r)) return r;
+  if (is_error(s = stage_out(&ctx->c, sb))) return s;
+  if (lambda && is_error(s = stage_out(&ctx->c, lb))) return s;
+  if (G64_out && !g_dev) {
+    if (is_error(s = cuda_ok(cudaMemcpyAsync(G64_out, G, (size_t)m * m * 8, cudaMemcpyDeviceToHost, c->stream))))
+      return s;
+    if (is_error(s = cuda_ok(cudaStreamSynchronize(c->stream)))) return s;
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------------------ test stream
+static tsk_status scw_common(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
+                             float* L, float* R, float* sigma, double* err) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !S) return TSK_ENULL;
+  if (B < 0 || m < 1 || n < 1 || k < 1 || k > m || r < 1) return TSK_EINVAL;
+  if (n % 4) return TSK_ESHAPE;
+  if (k > 128) return TSK_EINVAL;
+  tsk_status warn = TSK_OK;
+  if (r > k) {
+    r = k;
+    warn = TSK_WARN_RANK_CLAMPED;
+  }
+  if (r > std::min(m, n) || r > 64) return TSK_EINVAL;
+  if (B == 0) return warn;
+  Ctx* c = &ctx->c;
+  cudaSetDevice(c->device);
+  DevBuf sb;
+  tsk_status s = stage_slot(ctx, S, (size_t)k * m * 4, 2, sb, true);
+  if (is_error(s)) return s;
+  const float* Sd = reinterpret_cast<const float*>(sb.dev);
+  const bool a_dev = is_device_ptr(A);
+  const bool out_dev = (!L || is_device_ptr(L)) && (!R || is_device_ptr(R)) && (!sigma || is_device_ptr(sigma)) &&
+                       (!err || is_device_ptr(err));
+  if (a_dev && out_dev) {
+    s = tsk::scw_run(c, A, B, m, n, Sd, k, r, L, R, sigma, err);
+    return is_error(s) ? s : warn;
+  }
+  // host path: chunk over matrices, stage in / run / copy results out
+  const size_t mat = (size_t)m * n * 4;
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(((size_t)512 << 20) / mat));
+  chunk = std::min<int64_t>(chunk, B);
+  float* Ad = nullptr;
+  if (!a_dev) {
+    Ad = reinterpret_cast<float*>(c->workspace(tsk::WS_HOST_IN, (size_t)chunk * mat));
+    if (!Ad) return TSK_ENOMEM;
+  }
+  const size_t out_per = ((L ? (size_t)m * r * 4 : 0) + (R ? (size_t)n * r * 4 : 0) + (sigma ? (size_t)r * 4 : 0) +
+                          (err ? 8 : 0) + 64);
+  uint8_t* Od = reinterpret_cast<uint8_t*>(c->workspace(tsk::WS_HOST_OUT, (size_t)chunk * out_per + 256));
+  if (!Od) return TSK_ENOMEM;
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t bc = std::min<int64_t>(chunk, B - b0);
+    const float* Ac = A + (size_t)b0 * m * n;
+    if (!a_dev) {
+      if (is_error(s = cuda_ok(cudaMemcpyAsync(Ad, Ac, (size_t)bc * mat, cudaMemcpyHostToDevice, c->stream)))) return s;
+      Ac = Ad;
+    }
+    uint8_t* o = Od;
+    auto carve = [&](size_t bytes) {
+      uint8_t* p = o;
+      o += (bytes + 255) & ~size_t(255);
+      return p;
+    };
+    float* Lc = L ? (is_device_ptr(L) ? L + (size_t)b0 * m * r : reinterpret_cast<float*>(carve((size_t)bc * m * r * 4))) : nullptr;
+    float* Rc = R ? (is_device_ptr(R) ? R + (size_t)b0 * n * r : reinterpret_cast<float*>(carve((size_t)bc * n * r * 4))) : nullptr;
+    float* sc = sigma ? (is_device_ptr(sigma) ? sigma + (size_t)b0 * r : reinterpret_cast<float*>(carve((size_t)bc * r * 4))) : nullptr;
+    double* ec = err ? (is_device_ptr(err) ? err + b0 : reinterpret_cast<double*>(carve((size_t)bc * 8))) : nullptr;
+    if (is_error(s = tsk::scw_run(c, Ac, bc, m, n, Sd, k, r, Lc, Rc, sc, ec))) return s;
+    if (L && !is_device_ptr(L))
+      cudaMemcpyAsync(L + (size_t)b0 * m * r, Lc, (size_t)bc * m * r * 4, cudaMemcpyDeviceToHost, c->stream);
+    if (R && !is_device_ptr(R))
+      cudaMemcpyAsync(R + (size_t)b0 * n * r, Rc, (size_t)bc * n * r * 4, cudaMemcpyDeviceToHost, c->stream);
+    if (sigma && !is_device_ptr(sigma))
+      cudaMemcpyAsync(sigma + (size_t)b0 * r, sc, (size_t)bc * r * 4, cudaMemcpyDeviceToHost, c->stream);
+    if (err && !is_device_ptr(err)) cudaMemcpyAsync(err + b0, ec, (size_t)bc * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (is_error(s = cuda_ok(cudaStreamSynchronize(c->stream)))) return s;
+  }
+  return warn;
+}
+
+tsk_status sketch_apply_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
+                            float* L, float* R, float* sigma) {
+  return scw_common(ctx, A, B, m, n, S, k, r, L, R, sigma, nullptr);
+}
+
+tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
+                     double* err) {
+  if (!err) return TSK_ENULL;
+  return scw_common(ctx, A, B, m, n, S, k, r, nullptr, nullptr, nullptr, err);
+}
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// Small fp64 dense kernels for the eigensolver and SCW (CUDA cores; these are the
+// p x p / m x p pieces around the tensor-core products, latency- rather than
+// throughput-bound).  Deterministic: split reductions are summed in fixed order.
+#include <algorithm>
+#include <cmath>
+
+#include "dense64.cuh"
+#include "ptx.cuh"
+
+namespace tsk {
+
+// ---------------------------------------------------------------- C = X^T Y (contraction over rows)
+// X: [batch][m][p] (ldx), Y: [batch][m][q] (ldy), partial: [batch][splits][p][q]
+__global__ void gemm_tn_f64_kernel(const double* __restrict__ X, long long ldx, long long sx,
+                                   const double* __restrict__ Y, long long ldy, long long sy, int m, int p, int q,
+                                   int splits, double* __restrict__ part) {
+  __shared__ double Xs[32][33];
+  __shared__ double Ys[32][33];
+  const int b = blockIdx.z / splits;
+  const int sp = blockIdx.z % splits;
+  const int a0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 256 threads
+  const int r0 = (int)((long long)sp * m / splits), r1 = (int)((long long)(sp + 1) * m / splits);
+  const double* Xb = X + (size_t)b * sx;
+  const double* Yb = Y + (size_t)b * sy;
+  double acc[2][2] = {{0, 0}, {0, 0}};
+  for (int i0 = r0; i0 < r1; i0 += 32) {
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int ii = e >> 5, cc = e & 31;
+      const int i = i0 + ii;
+      Xs[ii][cc] = (i < r1 && a0 + cc < p) ? Xb[(size_t)i * ldx + a0 + cc] : 0.0;
+      Ys[ii][cc] = (i < r1 && c0 + cc < q) ? Yb[(size_t)i * ldy + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int ii = 0; ii < 32; ++ii) {
+      const double x0 = Xs[ii][ty * 2], x1 = Xs[ii][ty * 2 + 1];
+      const double y0 = Ys[ii][tx * 2], y1 = Ys[ii][tx * 2 + 1];
+      acc[0][0] += x0 * y0;
+      acc[0][1] += x0 * y1;
+      acc[1][0] += x1 * y0;
+      acc[1][1] += x1 * y1;
+    }
+    __syncthreads();
+  }
+  double* P = part + ((size_t)b * splits + sp) * p * q;
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int a = a0 + ty * 2 + u, c = c0 + tx * 2 + v;
+      if (a < p && c < q) P[(size_t)a * q + c] = acc[u][v];
+    }
+}
+
+__global__ void reduce_splits_kernel(const double* __restrict__ part, int splits, int p, int q, int batch, int sym,
+                                     double* __restrict__ C, long long ldc, long long sc) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long tot = (long long)batch * p * q;
+  if (idx >= tot) return;
+  const int b = (int)(idx / ((long long)p * q));
+  const int rem = (int)(idx % ((long long)p * q));
+  const int a = rem / q, c = rem % q;
+  const double* P = part + (size_t)b * splits * p * q;
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += P[(size_t)k * p * q + rem];
+  if (sym) {
+    double t = 0.0;
+    for (int k = 0; k < splits; ++k) t += P[(size_t)k * p * q + (size_t)c * q + a];
+    s = 0.5 * (s + t);
+  }
+  C[(size_t)b * sc + (size_t)a * ldc + c] = s;
+}
+
+tsk_status gemm_tn_f64(Ctx* ctx, const double* X, long long ldx, long long sx, const double* Y, long long ldy,
+                       long long sy, int m, int p, int q, int batch, double* C, long long ldc, long long sc, int sym,
+                       int ws_id) {
+  const int tiles = ((p + 31) / 32) * ((q + 31) / 32) * batch;
+  int splits = std::max(1, std::min((ctx->num_sms * 2 + tiles - 1) / tiles, std::max(1, m / 64)));
+  double* part = reinterpret_cast<double*>(ctx->workspace(ws_id, (size_t)batch * splits * p * q * sizeof(double)));
+  if (!part) return TSK_ENOMEM;
+  dim3 grid((q + 31) / 32, (p + 31) / 32, batch * splits);
+  gemm_tn_f64_kernel<<<grid, 256, 0, ctx->stream>>>(X, ldx, sx, Y, ldy, sy, m, p, q, splits, part);
+  const long long tot = (long long)batch * p * q;
+  reduce_splits_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, ctx->stream>>>(part, splits, p, q, batch, sym, C, ldc,
+                                                                                 sc);
+  ctx->count_launch(2);
+  return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
+}
+
+// ---------------------------------------------------------------- Y = alpha * Z W, optional column scale
+// Z: [batch][m][p] (ldz), W: [batch][p][q] (ldw, stride sw; sw = 0 broadcasts one W), Y: [batch][m][q]
+__global__ void gemm_nn_f64_kernel(const double* __restrict__ Z, long long ldz, long long sz,
+                                   const double* __restrict__ W, long long ldw, long long sw, int m, int p, int q,
+                                   const double* __restrict__ colscale, double* __restrict__ Y, long long ldy,
+                                   long long sy) {
+  __shared__ double Zs[64][33];
+  __shared__ double Ws[32][33];
+  const int b = blockIdx.z;
+  const int i0 = blockIdx.y * 64, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: ty 0..7 -> 8 rows each
+  const double* Zb = Z + (size_t)b * sz;
+  const double* Wb = W + (size_t)b * sw;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int a0 = 0; a0 < p; a0 += 32) {
+    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+      const int ii = e >> 5, aa = e & 31;
+      Zs[ii][aa] = (i0 + ii < m && a0 + aa < p) ? Zb[(size_t)(i0 + ii) * ldz + a0 + aa] : 0.0;
+    }
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int aa = e >> 5, cc = e & 31;
+      Ws[aa][cc] = (a0 + aa < p && c0 + cc < q) ? Wb[(size_t)(a0 + aa) * ldw + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int aa = 0; aa < 32; ++aa) {
+      const double w = Ws[aa][tx];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += Zs[ty * 8 + u][aa] * w;
+    }
+    __syncthreads();
+  }
+  const int c = c0 + tx;
+  if (c < q) {
+    const double s = colscale ? colscale[(size_t)b * q + c] : 1.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + ty * 8 + u;
+      if (i < m) Y[(size_t)b * sy + (size_t)i * ldy + c] = acc[u] * s;
+    }
+  }
+}
+
+tsk_status gemm_nn_f64(Ctx* ctx, const double* Z, long long ldz, long long sz, const double* W, long long ldw,
+                       long long sw, int m, int p, int q, int batch, const double* colscale, double* Y, long long ldy,
+                       long long sy) {
+  dim3 grid((q + 31) / 32, (m + 63) / 64, batch);
+  gemm_nn_f64_kernel<<<grid, 256, 0, ctx->stream>>>(Z, ldz, sz, W, ldw, sw, m, p, q, colscale, Y, ldy, sy);
+  ctx->count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
+}
+
+// ---------------------------------------------------------------- Cholesky C = L L^T and R^{-1} = L^{-T}
+// One CTA per matrix.  C: [batch][p][p] sym.  Rinv: [batch][p][p] upper triangular with
+// Q = Y Rinv orthonormal.  flag[b] = index+1 of the first failed pivot (0 = success).
+// A pivot fails if it is <= rel_tol * (largest original diagonal).
+__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ C, int p, double rel_tol,
+                                                        double* __restrict__ Rinv, int* __restrict__ flag,
+                                                        double* __restrict__ gscratch, int use_smem) {
+  extern __shared__ double csm[];
+  __shared__ double dmax;
+  __shared__ int fail;
+  const int b = blockIdx.x;
+  double* Lm = use_smem ? csm : gscratch + (size_t)b * p * p;  // row-major lower factor in place
+  const double* Cb = C + (size_t)b * p * p;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) Lm[e] = Cb[e];
+  if (threadIdx.x == 0) {
+    double d = 0;
+    for (int i = 0; i < p; ++i) d = fmax(d, Cb[(size_t)i * p + i]);
+    dmax = d;
+    fail = 0;
+  }
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    // pivot
+    if (threadIdx.x == 0) {
+      double d = Lm[(size_t)j * p + j];
+      if (!(d > rel_tol * dmax)) {
+        if (fail == 0) fail = j + 1;
+        d = fmax(dmax, 1e-300);  // keep going with a benign pivot; caller repairs
+      }
+      Lm[(size_t)j * p + j] = sqrt(d);
+    }
+    __syncthreads();
+    const double ljj = Lm[(size_t)j * p + j];
+    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) Lm[(size_t)i * p + j] /= ljj;
+    __syncthreads();
+    // trailing update of the lower triangle
+    const int nt = p - j - 1;
+    for (int e = threadIdx.x; e < nt * nt; e += blockDim.x) {
+      const int i = j + 1 + e / nt, l = j + 1 + e % nt;
+      if (l <= i) Lm[(size_t)i * p + l] -= Lm[(size_t)i * p + j] * Lm[(size_t)l * p + j];
+    }
+    __syncthreads();
+  }
+  // Linv (lower) by forward substitution, one column per thread; write Rinv = Linv^T (upper)
+  double* Rb = Rinv + (size_t)b * p * p;
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    // column c of Linv: x = L^{-1} e_c, x_i = 0 for i < c (only i >= c is stored)
+    for (int i = c; i < p; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) s -= Lm[(size_t)i * p + l] * Rb[(size_t)l * p + c];
+      Rb[(size_t)i * p + c] = s / Lm[(size_t)i * p + i];
+    }
+  }
+  __syncthreads();
+  // Rb currently holds Linv in row-major (Rb[i][c] = Linv[i][c], lower).  Transpose in place.
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e / p, c = e % p;
+    if (i > c) {
+      const double lo = Rb[(size_t)i * p + c];
+      Rb[(size_t)c * p + i] = lo;
+      Rb[(size_t)i * p + c] = 0.0;
+    }
+  }
+  if (threadIdx.x == 0) flag[b] = fail;
+}
+
+tsk_status chol_inv(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* Rinv, int* flag, int ws_id) {
+  const size_t need = (size_t)p * p * sizeof(double);
+  const int use_smem = need <= 200 * 1024;
+  double* scratch = nullptr;
+  if (!use_smem) {
+    scratch = reinterpret_cast<double*>(ctx->workspace(ws_id, need * batch));
+    if (!scratch) return TSK_ENOMEM;
+  }
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+      return TSK_ECUDA;
+    attr = true;
+  }
+  chol_inv_kernel<<<batch, 1024, use_smem ? need : 0, ctx->stream>>>(C, p, rel_tol, Rinv, flag, scratch, use_smem);
+  ctx->count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
+}
+
+}  // namespace tsk

@@ -1,0 +1,416 @@
+// Split-TF32 ("3xTF32") NT GEMM on tcgen05 tensor cores, the Gram hot loop of the
+// tensor-based sketch (G = A_(1) A_(1)^T = sum_d A_d A_d^T).
+//
+//   C[M x N] = sum_{z < D} X_z[M x n] * Y_z[N x n]^T          (fp64 result)
+//
+// X and Y are fp32, K-major (row-major with the contracted index contiguous) and are
+// addressed through 3-D TMA tensor maps [D][rows][n]; the contraction runs over the pair
+// (z, j) -- for the mode-1 Gram z = d (the stream index) and X = Y = the training stack,
+// so A_(1) is never materialised (its column order does not matter for G; reading c3).
+//
+// Precision: each 32-column K-chunk is split in shared memory into
+//   H = rna_tf32(x),  L = x - H   (exact in fp32)
+// and the tile accumulates H_X H_Y^T + H_X L_Y^T + L_X H_Y^T (L L^T dropped, ~2^-22 rel).
+// TMEM fp32 accumulation runs over bounded chains of `chain` chunks, is folded into
+// fp32 registers (round-to-nearest), and every `fold` chains into an fp64 per-unit partial.
+//
+// Work decomposition: the output is cut into 128x128 tiles (lower-triangle tiles only when
+// `sym`), K into S equal splits; unit u = s*T + t is handled by CTA (u mod grid).  A round
+// of `grid` consecutive units touches at most a few K-splits, so the CTAs of a round read the
+// same K window and the operands are served from L2 (HBM traffic ~1x the input).
+// A finalize kernel sums the S partials of each tile in fixed order (deterministic) and
+// mirrors the lower triangle for `sym`.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ptx.cuh"
+#include "tsk_internal.h"
+
+namespace tsk {
+
+constexpr int kBM = 128;            // tile rows (UMMA M)
+constexpr int kBN = 128;            // tile cols (UMMA N)
+constexpr int kBK = 32;             // fp32 elements per K-chunk = 128 B = one SW128 row
+constexpr int kStages = 3;
+constexpr int kTileBytes = kBM * kBK * 4;  // 16 KB
+constexpr int kStageBytes = 4 * kTileBytes;  // XH, XL, YH, YL
+constexpr int kThreads = 512;
+constexpr int kTmemCols = 256;      // two 128-column fp32 accumulators
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+struct GemmArgs {
+  int T;         // tiles
+  int nb;        // column blocks (general layout)
+  int sym;       // lower-triangle tiles of X X^T
+  int cps;       // K-chunks per slice = ceil(n / 32)
+  int S;         // K splits
+  long long Kc;  // chunks per tile = D * cps
+  int U;         // units = S * T
+  int chain;     // chunks per TMEM accumulation chain
+  int fold;      // chains per fp64 fold
+  int products;  // 3 = split-TF32 (production); 1 = H*H only (precision probe)
+  double* part;  // [U][128][128] fp64 partials
+};
+
+__device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& bi, int& bj) {
+  if (a.sym) {
+    int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    while (i * (i + 1) / 2 > t) --i;
+    bi = i;
+    bj = t - i * (i + 1) / 2;
+  } else {
+    bi = t / a.nb;
+    bj = t % a.nb;
+  }
+}
+
+__device__ __forceinline__ void unit_range(const GemmArgs& a, int u, int& t, long long& q0, long long& q1) {
+  t = u % a.T;
+  int s = u / a.T;
+  q0 = (long long)s * a.Kc / a.S;
+  q1 = (long long)(s + 1) * a.Kc / a.S;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
+                       const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = bars;                 // TMA -> transform
+  uint64_t* split = bars + kStages;      // transform -> MMA
+  uint64_t* empty = bars + 2 * kStages;  // MMA -> TMA
+  uint64_t* accf = bars + 3 * kStages;   // MMA -> epilogue (2 buffers)
+  uint64_t* acce = accf + 2;             // epilogue -> MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapX);
+    tma_prefetch_desc(&mapY);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&split[i], 4);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto stage_ptr = [&](int st, int which) { return smem + st * kStageBytes + which * kTileBytes; };
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        int t, bi, bj;
+        long long q0, q1;
+        unit_range(a, u, t, q0, q1);
+        tile_coords(a, t, bi, bj);
+        const bool diag = a.sym && bi == bj;
+        for (long long q = q0; q < q1; ++q) {
+          mbar_wait(&empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&full[st], diag ? kTileBytes : 2 * kTileBytes);
+          const int z = (int)(q / a.cps);
+          const int kc = (int)(q % a.cps) * kBK;
+          tma_load_3d(stage_ptr(st, 0), &mapX, &full[st], kc, bi * kBM, z);
+          if (!diag) tma_load_3d(stage_ptr(st, 2), &mapY, &full[st], kc, bj * kBN, z);
+          if (++st == kStages) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (elect_one()) {
+      const uint32_t idesc = idesc_tf32(kBM, kBN);
+      int st = 0;
+      uint32_t ph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        int t, bi, bj;
+        long long q0, q1;
+        unit_range(a, u, t, q0, q1);
+        tile_coords(a, t, bi, bj);
+        const bool diag = a.sym && bi == bj;
+        int cpos = 0;
+        for (long long q = q0; q < q1; ++q) {
+          if (cpos == 0) {
+            mbar_wait(&acce[ab], aph ^ 1);
+            tc_fence_after();
+          }
+          mbar_wait(&split[st], ph);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)(ab * kBN);
+          const uint64_t xh = sw128_kmajor_desc(smem_u32(stage_ptr(st, 0)));
+          const uint64_t xl = sw128_kmajor_desc(smem_u32(stage_ptr(st, 1)));
+          const uint64_t yh = diag ? xh : sw128_kmajor_desc(smem_u32(stage_ptr(st, 2)));
+          const uint64_t yl = diag ? xl : sw128_kmajor_desc(smem_u32(stage_ptr(st, 3)));
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32 >> 4);  // +32 B per K=8 step inside the swizzle atom
+            mma_tf32_ss(d_tmem, xh + adv, yh + adv, idesc, (cpos > 0 || kk > 0) ? 1u : 0u);
+            if (a.products == 3) {
+              mma_tf32_ss(d_tmem, xh + adv, yl + adv, idesc, 1u);
+              mma_tf32_ss(d_tmem, xl + adv, yh + adv, idesc, 1u);
+            }
+          }
+          mma_commit(&empty[st]);
+          if (++st == kStages) { st = 0; ph ^= 1; }
+          if (++cpos == a.chain || q + 1 == q1) {
+            mma_commit(&accf[ab]);
+            cpos = 0;
+            if (++ab == 2) { ab = 0; aph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ===================== split transform: x -> (H = rna_tf32(x), L = x - H) =====================
+    const int tt = threadIdx.x - 128;  // 0..127
+    int st = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      int t, bi, bj;
+      long long q0, q1;
+      unit_range(a, u, t, q0, q1);
+      tile_coords(a, t, bi, bj);
+      const bool diag = a.sym && bi == bj;
+      for (long long q = q0; q < q1; ++q) {
+        mbar_wait(&full[st], ph);
+        const int ntiles = diag ? 1 : 2;
+        for (int w = 0; w < ntiles; ++w) {
+          float4* hp = reinterpret_cast<float4*>(stage_ptr(st, 2 * w));
+          float4* lp = reinterpret_cast<float4*>(stage_ptr(st, 2 * w + 1));
+#pragma unroll
+          for (int i = 0; i < kTileBytes / 16 / 128; ++i) {
+            const int idx = i * 128 + tt;
+            float4 v = hp[idx];
+            float4 h, l;
+            uint32_t b;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.x)); h.x = __uint_as_float(b);
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.y)); h.y = __uint_as_float(b);
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.z)); h.z = __uint_as_float(b);
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.w)); h.w = __uint_as_float(b);
+            l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+            hp[idx] = h;
+            lp[idx] = l;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&split[st]);
+        if (++st == kStages) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue: TMEM chains -> fp32 registers -> fp64 partials =====================
+    const int e = warp - 8;
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int col0 = (e >> 2) * 64;
+    const int row = quad * 32 + lane;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      int t;
+      long long q0, q1;
+      unit_range(a, u, t, q0, q1);
+      const long long nchunks = q1 - q0;
+      const long long nchains = (nchunks + a.chain - 1) / a.chain;
+      float sum[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+      int cin = 0;
+      bool first_fold = true;
+      double* prow = a.part + (size_t)u * (kBM * kBN) + (size_t)row * kBN + col0;
+      for (long long c = 0; c < nchains; ++c) {
+        mbar_wait(&accf[ab], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kBN + col0);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + h * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acce[ab]);
+        if (++ab == 2) { ab = 0; aph ^= 1; }
+        if (++cin == a.fold || c + 1 == nchains) {
+#pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            double2* p2 = reinterpret_cast<double2*>(prow + i);
+            double2 v;
+            if (first_fold) {
+              v.x = (double)sum[i];
+              v.y = (double)sum[i + 1];
+            } else {
+              v = *p2;
+              v.x += (double)sum[i];
+              v.y += (double)sum[i + 1];
+            }
+            *p2 = v;
+            sum[i] = 0.f;
+            sum[i + 1] = 0.f;
+          }
+          first_fold = false;
+          cin = 0;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// Sum the S partials of every tile in fixed order; write fp64 (and optionally fp32) output.
+// sym: only i >= j is summed and mirrored to (j, i), so the result is exactly symmetric.
+__global__ void gemm_finalize_kernel(const double* __restrict__ part, int M, int N, int T, int nb, int S, int sym,
+                                     double* __restrict__ out64, long long ldo64, float* __restrict__ out32,
+                                     long long ldo32, int accumulate) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= M || j >= N) return;
+  if (sym && j > i) return;
+  const int bi = i / kBM, bj = j / kBN;
+  const int t = sym ? bi * (bi + 1) / 2 + bj : bi * nb + bj;
+  const size_t off = (size_t)(i % kBM) * kBN + (j % kBN);
+  double acc = 0.0;
+  for (int s = 0; s < S; ++s) acc += part[(size_t)(s * T + t) * (kBM * kBN) + off];
+  if (out64) {
+    double v = accumulate ? out64[(size_t)i * ldo64 + j] + acc : acc;
+    out64[(size_t)i * ldo64 + j] = v;
+    if (sym && i != j) out64[(size_t)j * ldo64 + i] = v;
+    acc = v;
+  }
+  if (out32) {
+    out32[(size_t)i * ldo32 + j] = (float)acc;
+    if (sym && i != j) out32[(size_t)j * ldo32 + i] = (float)acc;
+  }
+}
+
+// ------------------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D map over [slices][rows][inner] fp32, box [1][128][32], 128-byte swizzle, OOB -> 0.
+static bool make_map_3d(CUtensorMap* map, const float* base, int inner, int rows, long long slices,
+                        long long row_stride_elems, long long slice_stride_elems) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)slices};
+  cuuint64_t strides[2] = {(cuuint64_t)(row_stride_elems * 4), (cuuint64_t)(slice_stride_elems * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)kBM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Choose the number of K splits S so that S*T units fill the grid in near-equal rounds.
+static int choose_splits(int T, long long Kc, int sms, int min_chunks) {
+  int best_s = 1;
+  double best_eff = -1.0;
+  const long long smax = std::max(1LL, std::min<long long>(Kc / std::max(1, min_chunks), 256));
+  for (int s = 1; s <= smax; ++s) {
+    long long U = (long long)s * T;
+    long long rounds = (U + sms - 1) / sms;
+    double eff = (double)U / (double)(rounds * sms);
+    if (eff > best_eff + 0.01) {
+      best_eff = eff;
+      best_s = s;
+    }
+  }
+  return best_s;
+}
+
+tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
+  if (p.M <= 0 || p.N <= 0 || p.n <= 0 || p.D <= 0) return TSK_EINVAL;
+  if ((p.n % 4) || (p.x_row_stride % 4) || (p.y_row_stride % 4) || (p.x_slice_stride % 4) ||
+      (p.y_slice_stride % 4) || (reinterpret_cast<uintptr_t>(p.X) & 15) || (reinterpret_cast<uintptr_t>(p.Y) & 15))
+    return TSK_ESHAPE;
+  if (p.sym && (p.X != p.Y || p.M != p.N)) return TSK_EINVAL;
+  CUtensorMap mx, my;
+  if (!make_map_3d(&mx, p.X, p.n, p.M, p.D, p.x_row_stride, p.x_slice_stride)) return TSK_ECUDA;
+  if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) return TSK_ECUDA;
+
+  GemmArgs a{};
+  const int mb = (p.M + kBM - 1) / kBM;
+  const int nb = (p.N + kBN - 1) / kBN;
+  a.sym = p.sym;
+  a.nb = nb;
+  a.T = p.sym ? mb * (mb + 1) / 2 : mb * nb;
+  a.cps = (p.n + kBK - 1) / kBK;
+  a.Kc = (long long)p.D * a.cps;
+  a.S = p.splits > 0 ? p.splits : choose_splits(a.T, a.Kc, ctx->num_sms, p.min_chunks_per_unit > 0 ? p.min_chunks_per_unit : 8);
+  if (a.S > a.Kc) a.S = (int)a.Kc;
+  a.U = a.S * a.T;
+  a.chain = p.chain > 0 ? p.chain : 4;
+  a.fold = p.fold > 0 ? p.fold : 16;
+  a.products = p.products == 1 ? 1 : 3;
+  const size_t part_bytes = (size_t)a.U * kBM * kBN * sizeof(double);
+  double* part = reinterpret_cast<double*>(ctx->workspace(WS_GEMM_PARTIAL, part_bytes));
+  if (!part) return TSK_ENOMEM;
+  a.part = part;
+
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
+        cudaSuccess)
+      return TSK_ECUDA;
+    attr_set = true;
+  }
+  const int grid = std::min(a.U, ctx->num_sms);
+  gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(mx, my, a);
+  if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
+  ctx->count_launch();
+
+  dim3 fb(32, 8);
+  dim3 fg((p.N + 31) / 32, (p.M + 7) / 8);
+  gemm_finalize_kernel<<<fg, fb, 0, ctx->stream>>>(part, p.M, p.N, a.T, nb, a.S, p.sym, p.out64, p.ldo64, p.out32,
+                                                   p.ldo32, p.accumulate);
+  if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
+  ctx->count_launch();
+  if (p.info) {
+    p.info->splits = a.S;
+    p.info->units = a.U;
+    p.info->grid = grid;
+    p.info->tiles = a.T;
+  }
+  return TSK_OK;
+}
+
+}  // namespace tsk

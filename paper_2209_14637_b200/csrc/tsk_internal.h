@@ -1,0 +1,124 @@
+// Internal declarations of libtsketch (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/tsketch.h"
+
+struct tsk_ctx_s;
+
+namespace tsk {
+
+enum WorkspaceId {
+  WS_GEMM_PARTIAL = 0,
+  WS_EIG_A,      // fp64 m x p blocks
+  WS_EIG_B,
+  WS_EIG_C,
+  WS_EIG_Q32,    // fp32 p x m (Q^T for the tensor-core product)
+  WS_EIG_SMALL,  // fp64 p x p matrices, flags
+  WS_EIG_G32,    // fp32 copy of G
+  WS_HOST_IN,    // device staging of host inputs
+  WS_HOST_OUT,
+  WS_SCW_0,
+  WS_SCW_1,
+  WS_SCW_2,
+  WS_SCW_3,
+  WS_SCW_4,
+  WS_SCW_5,
+  WS_GRAM,       // fp64 Gram for sketch_train
+  WS_JACOBI,
+  WS_COUNT
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  void* ws[WS_COUNT] = {};
+  size_t ws_size[WS_COUNT] = {};
+  void* host_pinned = nullptr;  // small pinned scratch for flags / scalars
+  size_t host_pinned_size = 0;
+
+  // grow-only device workspace; returns nullptr on allocation failure
+  void* workspace(int id, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (ws_size[id] >= bytes) return ws[id];
+    if (ws[id]) {
+      cudaStreamSynchronize(stream);
+      cudaFree(ws[id]);
+      ws[id] = nullptr;
+      ws_size[id] = 0;
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    ws[id] = p;
+    ws_size[id] = bytes;
+    return p;
+  }
+  void* pinned(size_t bytes) {
+    if (host_pinned_size >= bytes) return host_pinned;
+    if (host_pinned) cudaFreeHost(host_pinned);
+    host_pinned = nullptr;
+    host_pinned_size = 0;
+    if (cudaMallocHost(&host_pinned, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    host_pinned_size = bytes;
+    return host_pinned;
+  }
+  void count_launch(int n = 1) { launches += n; }
+};
+
+struct GemmInfo {
+  int splits = 0, units = 0, grid = 0, tiles = 0;
+};
+
+// C[M x N] (+)= sum_{z<D} X_z Y_z^T   (fp32 K-major operands via 3-D TMA maps)
+struct GemmProblem {
+  const float* X = nullptr;
+  const float* Y = nullptr;
+  int M = 0, N = 0, n = 0;
+  long long D = 1;
+  long long x_row_stride = 0, x_slice_stride = 0;
+  long long y_row_stride = 0, y_slice_stride = 0;
+  int sym = 0;
+  double* out64 = nullptr;
+  long long ldo64 = 0;
+  float* out32 = nullptr;
+  long long ldo32 = 0;
+  int accumulate = 0;
+  int splits = 0;               // 0 = auto
+  int min_chunks_per_unit = 0;  // 0 = default
+  int chain = 0;                // 0 = default
+  int fold = 0;
+  int products = 3;
+  GemmInfo* info = nullptr;
+};
+
+tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p);
+
+// eigensolver (eig.cu)
+tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda, const tsk_train_opts* o,
+                      tsk_train_info* info);
+
+// SCW (scw.cu); all pointers device
+tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, int r, float* L,
+                   float* R, float* sigma, double* err);
+
+// batched symmetric PSD eigensolver (one-sided Jacobi), jacobi.cu
+// H: [batch][p][p] fp64 symmetric (row-major, read only).  W: [batch][p][p] fp64 eigenvectors as
+// COLUMNS (W[b][i][c] = component i of eigenvector c), lam: [batch][p] fp64 decreasing.
+tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam);
+
+}  // namespace tsk
+
+struct tsk_ctx_s {
+  tsk::Ctx c;
+};

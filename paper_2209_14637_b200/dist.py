@@ -1,0 +1,41 @@
+"""Data parallelism over the stream index d.
+
+Rank p of P owns the contiguous training range [floor(pD/P), floor((p+1)D/P)), accumulates
+its partial mode-1 Gram G_p = sum_{d in shard} A_d A_d^T on its GPU (``sketch_gram``), and
+one all-reduce (sum) of the m x m Gram over NCCL / NVLink gives G on every rank.  The
+eigensolver then runs redundantly on every rank; it is deterministic, so every rank holds
+the same S and no broadcast is needed.  The test stream is sharded by matrix with no
+communication (each rank computes the errors of its own test matrices).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(D: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous d-range of `rank` among `world` ranks: [floor(rank*D/world), floor((rank+1)*D/world))."""
+    if world < 1 or not (0 <= rank < world) or D < 0:
+        raise ValueError(f"bad shard request D={D} rank={rank} world={world}")
+    return (rank * D) // world, ((rank + 1) * D) // world
+
+
+def reduce_gram(G64: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the ranks' partial Grams in place (the only collective of the training path)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(G64, op=dist.ReduceOp.SUM, group=group)
+    return G64
+
+
+def train(A_local: torch.Tensor, k: int, group=None, opts=None, G64: Optional[torch.Tensor] = None):
+    """Algorithm 2 lines 1-2 over all ranks of `group`: local Gram of this rank's shard,
+    all-reduce, top-k eigenvectors.  Returns (S [k, m], lambda [k], info, status)."""
+    from . import sketch_gram, sketch_topk
+
+    G64, ginfo = sketch_gram(A_local, G64=G64, opts=opts)
+    reduce_gram(G64, group)
+    S, lam, info, st = sketch_topk(G64, k, opts=opts)
+    info.gram_splits, info.gram_tiles = ginfo.gram_splits, ginfo.gram_tiles
+    return S, lam, info, st
