@@ -1,0 +1,344 @@
+"""Benchmark of the tensor-based sketch hot path (arXiv 2209.14637) on B200.
+
+One step = one pass of the whole hot path over the configured stream:
+  local mode-1 Gram of this rank's training shard (3xTF32 tcgen05)  ->  NCCL all-reduce of G (N > 1)
+  ->  top-k eigenvectors (sketch S)  ->  batched SCW + per-matrix error on this rank's test shard.
+Metric (BASELINE.json): training matrices/s for sketch construction = D_train / step time (the
+step includes the test-stream SCW, so this is conservative); strong scaling (D_train fixed).
+
+  python bench.py [--gpus N --steps K --warmup W --config C4]        (torchrun for N > 1)
+  python bench.py --impl reference ...                                 (the float64 CPU oracle)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "training matrices/s for sketch construction"
+UNIT = "matrices/s"
+NOMINAL_TF32_OVER_BF16 = 1.1 / 2.25   # B200_PROFILING.md nominal dense ratio (tf32 1.1 PF, bf16 2.25 PF)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return mp, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload_desc(c, n_gpus):
+    return {"workload": f"{c.name}: m={c.m} n={c.n} D_train={c.D_train} D_test={c.D_test} k={c.k} r={c.r} "
+                        f"(BASELINE.json configs[3], frame-like synthetic stream)",
+            "m": c.m, "n": c.n, "D_train": c.D_train, "D_test": c.D_test, "k": c.k, "r": c.r,
+            "parallelism": f"dp{n_gpus} over the stream index d (one NCCL all-reduce of G)",
+            "l2_policy": f"inputs larger than L2 ({c.train_bytes / 1e9:.1f} GB training stream per step)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def dist_setup(n_gpus):
+    if n_gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        rank = int(os.environ["RANK"])
+        world = int(os.environ["WORLD_SIZE"])
+        local = int(os.environ.get("LOCAL_RANK", rank))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        return rank, world, local
+    torch.cuda.set_device(0)
+    return 0, 1, 0
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------------------ reference arm
+def cpu_oracle_run(c, A_s: np.ndarray, T_s: np.ndarray, budget_s=20.0):
+    """Time the float64 oracle (oracle/) as it stands on the host cores, on a bounded sample of
+    the workload: the Gram over the sample matrices (repeated until ~half the budget is spent),
+    one eigh of the m x m Gram, and SCW on the sample test matrices; the per-matrix rates are
+    extrapolated to one full step (D_train training + D_test test matrices)."""
+    import threadpoolctl
+    from oracle import scw as oscw
+    from oracle import tucker1
+
+    info = threadpoolctl.threadpool_info()
+    cores = max([i.get("num_threads", 1) for i in info] + [1])
+    G = np.zeros((c.m, c.m))
+    nd = 0
+    t0 = time.perf_counter()
+    while True:
+        G += tucker1.mode1_gram(A_s)
+        nd += A_s.shape[0]
+        if time.perf_counter() - t0 > budget_s * 0.5:
+            break
+    t_gram = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    S, lam = tucker1.top_k_eigen(G, c.k)
+    t_eig = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oscw.scw_errors(T_s, S, c.r)
+    t_scw = (time.perf_counter() - t0) / T_s.shape[0]
+    t_step = t_gram / nd * c.D_train + t_eig + t_scw * c.D_test
+    return {"value": c.D_train / t_step, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"fp64 Gram of {nd} training matrices ({A_s.shape[0]} distinct, {t_gram:.1f}s) + "
+                      f"eigh({c.m}) ({t_eig:.2f}s) + SCW of {T_s.shape[0]} test matrices ({t_scw * T_s.shape[0]:.1f}s), "
+                      f"rates extrapolated to the full step (D_train={c.D_train}, D_test={c.D_test}); numpy "
+                      f"float64 + {info[0].get('internal_api', '?') if info else '?'} BLAS",
+            "seconds_per_step": t_step}
+
+
+def run_reference(args, c):
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    A_s = datagen.generate(c, "train", 0, 8).double().numpy()
+    T_s = datagen.generate(c, "test", 0, 2).numpy()
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_run(c, A_s, T_s, budget_s=max(4.0, 90.0 / max(1, args.warmup + args.steps)))
+        if i >= args.warmup:
+            times.append(r)
+    value = statistics.median([t["value"] for t in times])
+    ms = 1e3 * statistics.median([t["seconds_per_step"] for t in times])
+    cb = dict(times[-1])
+    cb["value"] = value
+    cb.pop("seconds_per_step", None)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen, seed 0)",
+            "config": workload_desc(c, args.gpus), "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_tsketch(args, c):
+    import paper_2209_14637_b200 as tsk
+    from paper_2209_14637_b200.dist import reduce_gram, shard_range
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    d0, d1 = shard_range(c.D_train, rank, world)
+    t0, t1 = shard_range(c.D_test, rank, world)
+    A = datagen.generate(c, "train", d0, d1, device=dev)
+    T = datagen.generate(c, "test", t0, t1, device=dev)
+    G = torch.empty(c.m, c.m, dtype=torch.float64, device=dev)
+    err = torch.empty(t1 - t0, dtype=torch.float64, device=dev)
+    ctx = tsk.context(dev)
+    stream = torch.cuda.current_stream(dev)
+    A_host_sample = A[:8].double().cpu().numpy() if rank == 0 else None
+    T_host_sample = T[:2].cpu().numpy() if rank == 0 else None
+
+    ev = {k: [] for k in ("gram", "allreduce", "eig", "scw")}
+
+    def step(record):
+        es = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if record else None
+        if record:
+            es[0].record(stream)
+        tsk.sketch_gram(A, G64=G, ctx=ctx)
+        if record:
+            es[1].record(stream)
+        reduce_gram(G)
+        if record:
+            es[2].record(stream)
+        S, lam, info, st = tsk.sketch_topk(G, c.k, ctx=ctx)
+        if record:
+            es[3].record(stream)
+        if t1 > t0:
+            tsk.scw_error(T, S, c.r, out=err, ctx=ctx)
+        if record:
+            es[4].record(stream)
+        return es, info
+
+    for _ in range(args.warmup):
+        step(False)
+    barrier(world)
+    l0 = ctx.launches
+    clocks = ClockSampler(local) if rank == 0 else None
+    barrier(world)
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    recs = []
+    info = None
+    for _ in range(args.steps):
+        es, info = step(True)
+        recs.append(es)
+    e_end.record(stream)
+    barrier(world)
+    clk = clocks.stop() if clocks else None
+    launches = ctx.launches - l0
+    total_ms = max_over_ranks(e_start.elapsed_time(e_end), world)
+    for es in recs:
+        ev["gram"].append(es[0].elapsed_time(es[1]))
+        ev["allreduce"].append(es[1].elapsed_time(es[2]))
+        ev["eig"].append(es[2].elapsed_time(es[3]))
+        ev["scw"].append(es[3].elapsed_time(es[4]))
+    phases = {k: max_over_ranks(statistics.mean(v), world) for k, v in ev.items()}
+    ms_step = total_ms / args.steps
+    value = c.D_train * args.steps / (total_ms / 1e3)
+
+    # ---- end-to-end through the C ABI with HOST buffers (H2D/D2H inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        Ah = torch.empty(tuple(A.shape), dtype=torch.float32, pin_memory=True)
+        Ah.copy_(A)
+        Th = torch.empty(tuple(T.shape), dtype=torch.float32, pin_memory=True)
+        Th.copy_(T)
+        Gh = torch.empty(c.m, c.m, dtype=torch.float64).pin_memory()
+        errh = torch.empty(t1 - t0, dtype=torch.float64).pin_memory()
+        del A
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            tsk.sketch_gram(Ah, G64=Gh, ctx=ctx)           # host stack streamed through the library
+            if world > 1:
+                Gd = Gh.to(dev)
+                reduce_gram(Gd)
+                Gh.copy_(Gd)
+            S, lam, _, _ = tsk.sketch_topk(Gh, c.k, ctx=ctx)  # host G in, host S out
+            if t1 > t0:
+                tsk.scw_error(Th, S, c.r, out=errh, ctx=ctx)  # host test stack in, host errors out
+            return float(errh.sum()) if t1 > t0 else 0.0
+
+        e2e_step()
+        barrier(world)
+        tt = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier(world)
+        e2e_s = max_over_ranks(time.perf_counter() - tt, world) / args.e2e_steps
+        h2d = (d1 - d0) * c.m * c.n * 4 + (t1 - t0) * c.m * c.n * 4 + c.m * c.m * 8 * 2
+        d2h = c.m * c.m * 8 * 2 + c.k * c.m * 4 + (t1 - t0) * 8
+        e2e = {"value": c.D_train / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "seconds_per_step": e2e_s, "steps": args.e2e_steps,
+               "path": "C ABI with pinned host buffers: sketch_gram (H2D streamed, overlapped) -> sketch_topk "
+                       "(host G/S) -> scw_error (host tensors)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    mp, peak_kind = measured_peaks()
+    peak_tf32 = mp["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
+    dloc = d1 - d0
+    alg_flops = c.m * (c.m + 1) * c.n * dloc     # lower-triangle Gram, per launch (this rank's shard)
+    gram_ms = phases["gram"]
+    achieved = alg_flops / (gram_ms / 1e3) / 1e12
+    tiles = info.gram_tiles if info and info.gram_tiles else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config") == c.name and tj.get("D") == dloc:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf32, "traffic": traffic,
+                "kernel": "gemm_tf32x3_kernel (+ gemm_finalize_kernel), 3xTF32 lower-triangle Gram",
+                "algorithmic_flops_per_launch": alg_flops,
+                "peak_note": f"TF32 = {peak_kind} bf16 sustained {mp['bf16_tflops_sustained']} TF/s x nominal "
+                             f"1.1/2.25 (B200_PROFILING.md)",
+                "issued_frac": 3 * achieved / peak_tf32 * ((-(-c.m // 128) * (-(-c.m // 128) + 1) / 2 * 128 * 128)
+                                                           / (c.m * (c.m + 1) / 2)),
+                "gram_ms_per_launch": gram_ms}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core products, fp64 partial sums and small solves)",
+            "data": "synthetic (datagen C4 recipe, seed 0; paper datasets unavailable)",
+            "config": workload_desc(c, world), "phases_ms": phases,
+            "sketch_construction_matrices_per_s": c.D_train / ((phases["gram"] + phases["allreduce"] + phases["eig"]) / 1e3),
+            "test_matrices_per_s": c.D_test / (phases["scw"] / 1e3) if phases["scw"] > 0 else None,
+            "eig_iters": info.iters if info else None, "roofline": roofline, "clocks": clk,
+            "gpu_launches": launches, "e2e": e2e}
+    if args.cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_oracle_run(c, A_host_sample, T_host_sample, budget_s=args.cpu_budget)
+        line["cpu_baseline"].pop("seconds_per_step", None)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tsketch", choices=["tsketch", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    c = datagen.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, c)
+    else:
+        run_tsketch(args, c)
+
+
+if __name__ == "__main__":
+    main()

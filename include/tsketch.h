@@ -68,9 +68,9 @@ int64_t tsk_launch_count(tsk_ctx ctx);
 /* ---------------------------------------------------------------------- training */
 
 typedef struct {
-  int oversample;    /* block size p = min(m, k + oversample); default (<= 0): k + max(k, 16) */
+  int oversample;    /* block size p = min(m, k + oversample) <= 256; default (<= 0): 16 */
   int max_iters;     /* subspace iterations cap; default 300 */
-  double tol;        /* convergence: Ritz residual <= tol * theta_1 for the top k; default 1e-6 */
+  double tol;        /* convergence: Ritz residual <= tol * theta_1 for the top k; default 5e-7 */
   int dense_max_m;   /* m <= this: one dense Jacobi eigensolve of G; default 256 */
   int gemm_chain;    /* tuning: K-chunks per TMEM accumulation chain (0 = default) */
   int gemm_splits;   /* tuning: K splits of the Gram (0 = auto) */
@@ -116,9 +116,25 @@ tsk_status sketch_apply_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n
                             float* L, float* R, float* sigma);
 
 /* Per-matrix SCW error err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64, dense residual with an fp64
-   reduction, not ||A||^2 - sum sigma^2).  err: [B] fp64 (device or host). */
+   reduction, not ||A||^2 - sum sigma^2).  err: [B] fp64 (device or host).  B = 0 is a no-op and
+   then accepts NULL pointers (as does sketch_apply_scw). */
 tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
                      double* err);
+
+/* ---------------------------------------------------------------------- diagnostics */
+
+/* Diagnostic entry to the Gram kernel (tests / microbenchmarks only; not part of the method):
+   same contract as sketch_gram (device pointers only, accumulate = 0) with
+     mode bit 0: skip the in-shared-memory hi/lo split (the MMA consumes the raw fp32 tiles),
+     mode bit 1: issue only the H*H^T product (1xTF32),
+   chain / splits as in tsk_train_opts (0 = default). */
+tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int mode, int chain,
+                          int splits);
+
+/* Diagnostic: the batched symmetric eigensolver used inside sketch_topk / SCW (device pointers).
+   H [batch][p][p] fp64 symmetric (row-major); W [batch][p][p] eigenvectors as columns; lam
+   [batch][p] eigenvalues, decreasing; sweeps [batch] (may be NULL) Jacobi sweeps used.  p <= 256. */
+tsk_status tsk_eig_probe(tsk_ctx ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps);
 
 #ifdef __cplusplus
 }

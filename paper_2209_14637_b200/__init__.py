@@ -30,7 +30,7 @@ STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVER
 
 # every symbol include/tsketch.h declares (checked by tests/test_abi.py on CPU)
 EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_status_string", "tsk_launch_count",
-            "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error"]
+            "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "tsk_gram_probe", "tsk_eig_probe"]
 
 
 class TskError(RuntimeError):
@@ -77,8 +77,10 @@ def lib() -> ctypes.CDLL:
         L.sketch_train.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, f64p, vp, vp]
         L.sketch_apply_scw.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, i32, f32p, f32p, f32p]
         L.scw_error.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, i32, f64p]
+        L.tsk_gram_probe.argtypes = [vp, f32p, i64, i32, i32, f64p, i32, i32, i32]
+        L.tsk_eig_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
-                  "sketch_train", "sketch_apply_scw", "scw_error"):
+                  "sketch_train", "sketch_apply_scw", "scw_error", "tsk_gram_probe", "tsk_eig_probe"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -259,6 +261,30 @@ def scw_error(A: torch.Tensor, S: torch.Tensor, r: int, out: Optional[torch.Tens
     err = out if out is not None else _alloc((B,), torch.float64, A)
     _check(lib().scw_error(ctx.handle, _ptr(A), B, m, n, _ptr(S), k, r, _ptr(err)), "scw_error")
     return err
+
+
+def tsk_gram_probe(A: torch.Tensor, mode: int = 0, chain: int = 0, splits: int = 0, G64=None,
+                   ctx: Optional[Context] = None) -> torch.Tensor:
+    """Diagnostic Gram launch (see include/tsketch.h): mode bit0 = raw tiles, bit1 = H*H only."""
+    _need(A, torch.float32, "A", 3)
+    D, m, n = A.shape
+    ctx = ctx or context(A.device)
+    G64 = G64 if G64 is not None else torch.empty((m, m), dtype=torch.float64, device=A.device)
+    _check(lib().tsk_gram_probe(ctx.handle, _ptr(A), D, m, n, _ptr(G64), mode, chain, splits), "tsk_gram_probe")
+    return G64
+
+
+def tsk_eig_probe(H: torch.Tensor, ctx: Optional[Context] = None):
+    """Diagnostic: batched symmetric eigensolver (include/tsketch.h).  H [B, p, p] fp64 cuda.
+    Returns (W [B, p, p] eigenvectors as columns, lam [B, p] decreasing, sweeps [B])."""
+    _need(H, torch.float64, "H", 3)
+    B, p, _ = H.shape
+    ctx = ctx or context(H.device)
+    W = torch.empty_like(H)
+    lam = torch.empty((B, p), dtype=torch.float64, device=H.device)
+    sw = torch.empty((B,), dtype=torch.int32, device=H.device)
+    _check(lib().tsk_eig_probe(ctx.handle, _ptr(H), p, B, _ptr(W), _ptr(lam), _ptr(sw)), "tsk_eig_probe")
+    return W, lam, sw
 
 
 from .dist import shard_range, train  # noqa: E402,F401

@@ -292,7 +292,7 @@ tsk_status sketch_topk(tsk_ctx ctx, const double* G64, int m, int k, float* S, d
   if (!ctx) return TSK_ENULL;
   if (!G64 || !S) return TSK_ENULL;
   if (m < 1 || k < 1 || k > m) return TSK_EINVAL;
-  if (m > 256 && k > 192) return TSK_EINVAL;
+  if (m > 256 && k + 16 > 256) return TSK_EINVAL;  // Rayleigh-Ritz block p = k + 16 <= 256
   cudaSetDevice(ctx->c.device);
   DevBuf g, sb, lb;
   tsk_status s = stage_slot(ctx, G64, (size_t)m * m * 8, 0, g, true);
@@ -313,7 +313,7 @@ tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, in
   if (!ctx) return TSK_ENULL;
   if (!A || !S) return TSK_ENULL;
   if (D < 1 || m < 1 || n < 1 || k < 1 || k > m) return TSK_EINVAL;
-  if (m > 256 && k > 192) return TSK_EINVAL;
+  if (m > 256 && k + 16 > 256) return TSK_EINVAL;  // Rayleigh-Ritz block p = k + 16 <= 256
   if (n % 4) return TSK_ESHAPE;
   Ctx* c = &ctx->c;
   cudaSetDevice(c->device);
@@ -351,8 +351,8 @@ tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, in
 static tsk_status scw_common(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
                              float* L, float* R, float* sigma, double* err) {
   if (!ctx) return TSK_ENULL;
-  if (!A || !S) return TSK_ENULL;
   if (B < 0 || m < 1 || n < 1 || k < 1 || k > m || r < 1) return TSK_EINVAL;
+  if (B > 0 && (!A || !S)) return TSK_ENULL;
   if (n % 4) return TSK_ESHAPE;
   if (k > 128) return TSK_EINVAL;
   tsk_status warn = TSK_OK;
@@ -425,8 +425,45 @@ tsk_status sketch_apply_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n
 
 tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
                      double* err) {
-  if (!err) return TSK_ENULL;
+  if (!err && B > 0) return TSK_ENULL;
   return scw_common(ctx, A, B, m, n, S, k, r, nullptr, nullptr, nullptr, err);
+}
+
+tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int mode, int chain,
+                          int splits) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !G64) return TSK_ENULL;
+  if (D < 1 || m < 1 || n < 1) return TSK_EINVAL;
+  if (n % 4) return TSK_ESHAPE;
+  if (!is_device_ptr(A) || !is_device_ptr(G64)) return TSK_EINVAL;
+  tsk::GemmProblem p;
+  p.X = A;
+  p.Y = A;
+  p.M = m;
+  p.N = m;
+  p.n = n;
+  p.D = D;
+  p.x_row_stride = n;
+  p.x_slice_stride = (long long)m * n;
+  p.y_row_stride = n;
+  p.y_slice_stride = (long long)m * n;
+  p.sym = 1;
+  p.out64 = G64;
+  p.ldo64 = m;
+  p.chain = chain;
+  p.splits = splits;
+  p.raw = mode & 1;
+  p.products = (mode & 2) ? 1 : 3;
+  return tsk::gemm_tf32x3(&ctx->c, p);
+}
+
+tsk_status tsk_eig_probe(tsk_ctx ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps) {
+  if (!ctx) return TSK_ENULL;
+  if (!H || !W || !lam) return TSK_ENULL;
+  if (p < 1 || p > 256 || batch < 0) return TSK_EINVAL;
+  if (!is_device_ptr(H) || !is_device_ptr(W) || !is_device_ptr(lam) || (sweeps && !is_device_ptr(sweeps)))
+    return TSK_EINVAL;
+  return tsk::jacobi_eig_batched(&ctx->c, H, p, batch, W, lam, sweeps, 1e-13);
 }
 
 }  // extern "C"

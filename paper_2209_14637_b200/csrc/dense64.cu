@@ -9,6 +9,20 @@
 
 namespace tsk {
 
+// global -> shared copy of n doubles by nthreads threads, 8 loads in flight per thread
+__device__ __forceinline__ void copy_to_shared(double* dst, const double* __restrict__ src, int n, int tid,
+                                               int nthreads) {
+  int e = tid;
+  for (; e + 7 * nthreads < n; e += 8 * nthreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = src[e + u * nthreads];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dst[e + u * nthreads] = v[u];
+  }
+  for (; e < n; e += nthreads) dst[e] = src[e];
+}
+
 // ---------------------------------------------------------------- C = X^T Y (contraction over rows)
 // X: [batch][m][p] (ldx), Y: [batch][m][q] (ldy), partial: [batch][splits][p][q]
 __global__ void gemm_tn_f64_kernel(const double* __restrict__ X, long long ldx, long long sx,
@@ -140,21 +154,25 @@ tsk_status gemm_nn_f64(Ctx* ctx, const double* Z, long long ldz, long long sz, c
   return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
 }
 
-// ---------------------------------------------------------------- Cholesky C = L L^T and R^{-1} = L^{-T}
-// One CTA per matrix.  C: [batch][p][p] sym.  Rinv: [batch][p][p] upper triangular with
-// Q = Y Rinv orthonormal.  flag[b] = index+1 of the first failed pivot (0 = success).
-// A pivot fails if it is <= rel_tol * (largest original diagonal).
-__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ C, int p, double rel_tol,
-                                                        double* __restrict__ Rinv, int* __restrict__ flag,
-                                                        double* __restrict__ gscratch, int use_smem) {
+// ---------------------------------------------------------------- Cholesky C = L L^T
+// One CTA of 256 threads per matrix, factor in shared memory (global scratch if too large).
+// Right-looking: p dependent steps; the trailing update of step j is spread over all threads
+// as a flat list of lower-triangle entries.  L: [batch][p][p] lower (row-major, upper = 0).
+// On failure flag[b] = index+1 of the first pivot <= rel_tol * max diag (untouched on success:
+// the caller clears it); the factorisation continues with a benign pivot, the caller repairs.
+constexpr int kCholThreads = 256;
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(const double* __restrict__ C, int p, double rel_tol,
+                                                            double* __restrict__ L, int* __restrict__ flag,
+                                                            double* __restrict__ gscratch, int use_smem) {
   extern __shared__ double csm[];
   __shared__ double dmax;
   __shared__ int fail;
   const int b = blockIdx.x;
-  double* Lm = use_smem ? csm : gscratch + (size_t)b * p * p;  // row-major lower factor in place
+  const int tid = threadIdx.x;
+  double* Lm = use_smem ? csm : gscratch + (size_t)b * p * p;
   const double* Cb = C + (size_t)b * p * p;
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) Lm[e] = Cb[e];
-  if (threadIdx.x == 0) {
+  copy_to_shared(Lm, Cb, p * p, tid, kCholThreads);
+  if (tid == 0) {
     double d = 0;
     for (int i = 0; i < p; ++i) d = fmax(d, Cb[(size_t)i * p + i]);
     dmax = d;
@@ -162,51 +180,68 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
   }
   __syncthreads();
   for (int j = 0; j < p; ++j) {
-    // pivot
-    if (threadIdx.x == 0) {
-      double d = Lm[(size_t)j * p + j];
-      if (!(d > rel_tol * dmax)) {
-        if (fail == 0) fail = j + 1;
-        d = fmax(dmax, 1e-300);  // keep going with a benign pivot; caller repairs
+    double d = Lm[(size_t)j * p + j];
+    if (!(d > rel_tol * dmax)) {
+      if (tid == 0 && fail == 0) fail = j + 1;
+      d = fmax(dmax, 1e-300);
+    }
+    const double inv = rsqrt(d);
+    for (int i = j + 1 + tid; i < p; i += kCholThreads) Lm[(size_t)i * p + j] *= inv;
+    __syncthreads();
+    if (tid == 0) Lm[(size_t)j * p + j] = d * inv;
+    // trailing lower triangle (i >= l > j): 16 x 16 thread grid, rows strided by 16, cols by 16
+    {
+      const int ty = tid >> 4, tx = tid & 15;
+      for (int i = j + 1 + ty; i < p; i += 16) {
+        const double lij = Lm[(size_t)i * p + j];
+        double* row = Lm + (size_t)i * p;
+        for (int l = j + 1 + tx; l <= i; l += 16) row[l] -= lij * Lm[(size_t)l * p + j];
       }
-      Lm[(size_t)j * p + j] = sqrt(d);
-    }
-    __syncthreads();
-    const double ljj = Lm[(size_t)j * p + j];
-    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) Lm[(size_t)i * p + j] /= ljj;
-    __syncthreads();
-    // trailing update of the lower triangle
-    const int nt = p - j - 1;
-    for (int e = threadIdx.x; e < nt * nt; e += blockDim.x) {
-      const int i = j + 1 + e / nt, l = j + 1 + e % nt;
-      if (l <= i) Lm[(size_t)i * p + l] -= Lm[(size_t)i * p + j] * Lm[(size_t)l * p + j];
     }
     __syncthreads();
   }
-  // Linv (lower) by forward substitution, one column per thread; write Rinv = Linv^T (upper)
-  double* Rb = Rinv + (size_t)b * p * p;
-  for (int c = threadIdx.x; c < p; c += blockDim.x) {
-    // column c of Linv: x = L^{-1} e_c, x_i = 0 for i < c (only i >= c is stored)
-    for (int i = c; i < p; ++i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int l = c; l < i; ++l) s -= Lm[(size_t)i * p + l] * Rb[(size_t)l * p + c];
-      Rb[(size_t)i * p + c] = s / Lm[(size_t)i * p + i];
-    }
+  double* Lb = L + (size_t)b * p * p;
+  for (int e = tid; e < p * p; e += kCholThreads) {
+    const int i = e / p, l = e % p;
+    Lb[e] = (l <= i) ? Lm[e] : 0.0;
   }
-  __syncthreads();
-  // Rb currently holds Linv in row-major (Rb[i][c] = Linv[i][c], lower).  Transpose in place.
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
-    const int i = e / p, c = e % p;
-    if (i > c) {
-      const double lo = Rb[(size_t)i * p + c];
-      Rb[(size_t)c * p + i] = lo;
-      Rb[(size_t)i * p + c] = 0.0;
-    }
-  }
-  if (threadIdx.x == 0) flag[b] = fail;
+  if (tid == 0 && fail) flag[b] = fail;
 }
 
-tsk_status chol_inv(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* Rinv, int* flag, int ws_id) {
+// ---------------------------------------------------------------- Q = Y L^{-T}  (row-parallel)
+// Each thread solves q L^T = y for one row of Y (forward substitution over columns), with L in
+// shared memory (all threads read the same L entry at the same time: broadcast) and its own
+// q row in a padded shared-memory slot.
+__global__ void trsm_rlt_kernel(const double* __restrict__ Y, const double* __restrict__ L, int m, int p,
+                                int rows_per_block, double* __restrict__ Q) {
+  extern __shared__ double tsm[];
+  double* Ls = tsm;                         // [p][p]
+  const int ld = p | 1;                     // odd stride in doubles for the per-thread rows
+  double* qs = tsm + (size_t)p * p;         // [rows_per_block][ld]
+  copy_to_shared(Ls, L, p * p, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int row = blockIdx.x * rows_per_block + threadIdx.x;
+  if (threadIdx.x >= rows_per_block || row >= m) return;
+  double* q = qs + (size_t)threadIdx.x * ld;
+  const double* y = Y + (size_t)row * p;
+  for (int c = 0; c < p; ++c) {
+    const double* Lc = Ls + (size_t)c * p;
+    double s0 = y[c], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int a = 0;
+    for (; a + 3 < c; a += 4) {
+      s0 -= q[a] * Lc[a];
+      s1 -= q[a + 1] * Lc[a + 1];
+      s2 -= q[a + 2] * Lc[a + 2];
+      s3 -= q[a + 3] * Lc[a + 3];
+    }
+    for (; a < c; ++a) s0 -= q[a] * Lc[a];
+    q[c] = ((s0 + s1) + (s2 + s3)) / Lc[c];
+  }
+  double* out = Q + (size_t)row * p;
+  for (int c = 0; c < p; ++c) out[c] = q[c];
+}
+
+tsk_status chol(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* L, int* flag, int ws_id) {
   const size_t need = (size_t)p * p * sizeof(double);
   const int use_smem = need <= 200 * 1024;
   double* scratch = nullptr;
@@ -216,11 +251,25 @@ tsk_status chol_inv(Ctx* ctx, const double* C, int p, int batch, double rel_tol,
   }
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+    if (cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(trsm_rlt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) != cudaSuccess)
       return TSK_ECUDA;
     attr = true;
   }
-  chol_inv_kernel<<<batch, 1024, use_smem ? need : 0, ctx->stream>>>(C, p, rel_tol, Rinv, flag, scratch, use_smem);
+  chol_kernel<<<batch, kCholThreads, use_smem ? need : 0, ctx->stream>>>(C, p, rel_tol, L, flag, scratch, use_smem);
+  ctx->count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
+}
+
+tsk_status trsm_rlt(Ctx* ctx, const double* Y, const double* L, int m, int p, double* Q) {
+  const size_t lbytes = (size_t)p * p * 8;
+  const int ld = p | 1;
+  if (lbytes + (size_t)32 * ld * 8 > 220 * 1024) return TSK_EINVAL;  // p <= ~150
+  // one warp per block: the kernel is shared-memory-bandwidth bound per SM, so spread rows
+  const int rows = 32;
+  const size_t smem = lbytes + (size_t)rows * ld * 8;
+  // 256 threads copy L into shared memory; the first `rows` of them then solve one row each
+  trsm_rlt_kernel<<<(m + rows - 1) / rows, 256, smem, ctx->stream>>>(Y, L, m, p, rows, Q);
   ctx->count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
 }

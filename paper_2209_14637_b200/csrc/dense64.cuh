@@ -12,6 +12,8 @@ tsk_status gemm_tn_f64(Ctx* ctx, const double* X, long long ldx, long long sx, c
 tsk_status gemm_nn_f64(Ctx* ctx, const double* Z, long long ldz, long long sz, const double* W, long long ldw,
                        long long sw, int m, int p, int q, int batch, const double* colscale, double* Y, long long ldy,
                        long long sy);
-// Cholesky C = L L^T and Rinv = L^{-T} (upper); flag[b] = first failed pivot + 1 (0 = ok)
-tsk_status chol_inv(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* Rinv, int* flag, int ws_id);
+// Cholesky C[b] = L L^T (L lower, row-major); on failure flag[b] = first failed pivot + 1 (sticky)
+tsk_status chol(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* L, int* flag, int ws_id);
+// Q = Y L^{-T} (Y, Q: m x p row-major; L: p x p lower), i.e. Q R = Y with R = L^T; p <= ~150
+tsk_status trsm_rlt(Ctx* ctx, const double* Y, const double* L, int m, int p, double* Q);
 }  // namespace tsk

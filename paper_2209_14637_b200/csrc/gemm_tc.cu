@@ -8,11 +8,11 @@
 // (z, j) -- for the mode-1 Gram z = d (the stream index) and X = Y = the training stack,
 // so A_(1) is never materialised (its column order does not matter for G; reading c3).
 //
-// Precision: each 32-column K-chunk is split in shared memory into
-//   H = rna_tf32(x),  L = x - H   (exact in fp32)
-// and the tile accumulates H_X H_Y^T + H_X L_Y^T + L_X H_Y^T (L L^T dropped, ~2^-22 rel).
-// TMEM fp32 accumulation runs over bounded chains of `chain` chunks, is folded into
-// fp32 registers (round-to-nearest), and every `fold` chains into an fp64 per-unit partial.
+// Precision: each 32-column K-chunk x is split into
+//   H = trunc_tf32(x) (the tensor core's own fp32->tf32 conversion),  L = x - H (exact)
+// and the tile accumulates H_X H_Y^T + H_X L_Y^T + L_X H_Y^T (L L^T dropped, ~2^-21 rel).
+// TMEM fp32 accumulation (truncating) runs over bounded chains of `chain` chunks, is folded
+// into fp32 registers (round-to-nearest), and every `fold` chains into an fp64 partial.
 //
 // Work decomposition: the output is cut into 128x128 tiles (lower-triangle tiles only when
 // `sym`), K into S equal splits; unit u = s*T + t is handled by CTA (u mod grid).  A round
@@ -33,12 +33,12 @@ namespace tsk {
 constexpr int kBM = 128;            // tile rows (UMMA M)
 constexpr int kBN = 128;            // tile cols (UMMA N)
 constexpr int kBK = 32;             // fp32 elements per K-chunk = 128 B = one SW128 row
-constexpr int kStages = 3;
+constexpr int kRawStages = 5;       // TMA ring: raw fp32 tiles of X and Y (the raw tile IS the hi part)
+constexpr int kLoStages = 2;        // transform ring: lo parts L = x - trunc_tf32(x)
 constexpr int kTileBytes = kBM * kBK * 4;  // 16 KB
-constexpr int kStageBytes = 4 * kTileBytes;  // XH, XL, YH, YL
 constexpr int kThreads = 512;
-constexpr int kTmemCols = 256;      // two 128-column fp32 accumulators
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kTmemCols = 512;      // 2 buffers x {H H^T, cross} x 128 fp32 columns
+constexpr int kSmemBytes = (kRawStages + kLoStages) * 2 * kTileBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 struct GemmArgs {
   int T;         // tiles
@@ -51,6 +51,7 @@ struct GemmArgs {
   int chain;     // chunks per TMEM accumulation chain
   int fold;      // chains per fp64 fold
   int products;  // 3 = split-TF32 (production); 1 = H*H only (precision probe)
+  int raw;       // diagnostics: 1 = skip the split transform (the lo buffers are not written)
   double* part;  // [U][128][128] fp64 partials
 };
 
@@ -74,17 +75,29 @@ __device__ __forceinline__ void unit_range(const GemmArgs& a, int u, int& t, lon
   q1 = (long long)(s + 1) * a.Kc / a.S;
 }
 
+// Warp roles (16 warps): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle,
+// 4-7 split transform, 8-15 epilogue.
+//
+// The tensor core reads fp32 operands of kind::tf32 by TRUNCATING them to tf32 (measured on
+// B200, scripts/gram_probe.py), so the raw TMA tile is used directly as the hi part
+// H = trunc_tf32(x) and only L = x - H (exact in fp32) is produced in shared memory.
+// Products go to two TMEM accumulators per buffer: ACC_HH += H_X H_Y^T and
+// ACC_X += H_X L_Y^T + L_X H_Y^T (2^-10-scaled terms: their truncating accumulation error is
+// negligible), which divides the dominant accumulation error by three at equal chain length.
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                        const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* full = bars;                 // TMA -> transform
-  uint64_t* split = bars + kStages;      // transform -> MMA
-  uint64_t* empty = bars + 2 * kStages;  // MMA -> TMA
-  uint64_t* accf = bars + 3 * kStages;   // MMA -> epilogue (2 buffers)
-  uint64_t* acce = accf + 2;             // epilogue -> MMA
+  uint8_t* raw_base = smem;                                        // [kRawStages][X|Y]
+  uint8_t* lo_base = smem + kRawStages * 2 * kTileBytes;           // [kLoStages][XL|YL]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lo_base + kLoStages * 2 * kTileBytes);
+  uint64_t* rfull = bars;                        // TMA -> transform / MMA
+  uint64_t* rempty = rfull + kRawStages;         // MMA -> TMA
+  uint64_t* lfull = rempty + kRawStages;         // transform -> MMA
+  uint64_t* lempty = lfull + kLoStages;          // MMA -> transform
+  uint64_t* accf = lempty + kLoStages;           // MMA -> epilogue (2 buffers)
+  uint64_t* acce = accf + 2;                     // epilogue -> MMA
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
 
   const int warp = threadIdx.x >> 5;
@@ -93,10 +106,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapX);
     tma_prefetch_desc(&mapY);
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&split[i], 4);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < kRawStages; ++i) {
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], 1);
+    }
+    for (int i = 0; i < kLoStages; ++i) {
+      mbar_init(&lfull[i], 4);
+      mbar_init(&lempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&accf[i], 1);
@@ -110,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto stage_ptr = [&](int st, int which) { return smem + st * kStageBytes + which * kTileBytes; };
+  auto raw_ptr = [&](int st, int which) { return raw_base + (st * 2 + which) * kTileBytes; };
+  auto lo_ptr = [&](int st, int which) { return lo_base + (st * 2 + which) * kTileBytes; };
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -124,13 +141,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(a, t, bi, bj);
         const bool diag = a.sym && bi == bj;
         for (long long q = q0; q < q1; ++q) {
-          mbar_wait(&empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&full[st], diag ? kTileBytes : 2 * kTileBytes);
+          mbar_wait(&rempty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&rfull[st], diag ? kTileBytes : 2 * kTileBytes);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
-          tma_load_3d(stage_ptr(st, 0), &mapX, &full[st], kc, bi * kBM, z);
-          if (!diag) tma_load_3d(stage_ptr(st, 2), &mapY, &full[st], kc, bj * kBN, z);
-          if (++st == kStages) { st = 0; ph ^= 1; }
+          tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
+          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * kBN, z);
+          if (++st == kRawStages) { st = 0; ph ^= 1; }
         }
       }
     }
@@ -138,8 +155,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== MMA issuer (one thread) =====================
     if (elect_one()) {
       const uint32_t idesc = idesc_tf32(kBM, kBN);
-      int st = 0;
-      uint32_t ph = 0;
+      int rs = 0, ls = 0;
+      uint32_t rph = 0, lph = 0;
       int ab = 0;
       uint32_t aph = 0;
       for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
@@ -154,24 +171,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&acce[ab], aph ^ 1);
             tc_fence_after();
           }
-          mbar_wait(&split[st], ph);
+          if (a.products == 3) mbar_wait(&lfull[ls], lph);  // implies the raw stage landed
+          else mbar_wait(&rfull[rs], rph);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + (uint32_t)(ab * kBN);
-          const uint64_t xh = sw128_kmajor_desc(smem_u32(stage_ptr(st, 0)));
-          const uint64_t xl = sw128_kmajor_desc(smem_u32(stage_ptr(st, 1)));
-          const uint64_t yh = diag ? xh : sw128_kmajor_desc(smem_u32(stage_ptr(st, 2)));
-          const uint64_t yl = diag ? xl : sw128_kmajor_desc(smem_u32(stage_ptr(st, 3)));
+          const uint32_t d_hh = tmem_base + (uint32_t)(ab * 2 * kBN);
+          const uint32_t d_x = d_hh + kBN;
+          const uint64_t xh = sw128_kmajor_desc(smem_u32(raw_ptr(rs, 0)));
+          const uint64_t yh = diag ? xh : sw128_kmajor_desc(smem_u32(raw_ptr(rs, 1)));
+          const uint64_t xl = sw128_kmajor_desc(smem_u32(lo_ptr(ls, 0)));
+          const uint64_t yl = diag ? xl : sw128_kmajor_desc(smem_u32(lo_ptr(ls, 1)));
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32 >> 4);  // +32 B per K=8 step inside the swizzle atom
-            mma_tf32_ss(d_tmem, xh + adv, yh + adv, idesc, (cpos > 0 || kk > 0) ? 1u : 0u);
+            const uint32_t acc = (cpos > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_ss(d_hh, xh + adv, yh + adv, idesc, acc);
             if (a.products == 3) {
-              mma_tf32_ss(d_tmem, xh + adv, yl + adv, idesc, 1u);
-              mma_tf32_ss(d_tmem, xl + adv, yh + adv, idesc, 1u);
+              mma_tf32_ss(d_x, xh + adv, yl + adv, idesc, acc);
+              mma_tf32_ss(d_x, xl + adv, yh + adv, idesc, 1u);
             }
           }
-          mma_commit(&empty[st]);
-          if (++st == kStages) { st = 0; ph ^= 1; }
+          mma_commit(&rempty[rs]);
+          if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+          if (a.products == 3) {
+            mma_commit(&lempty[ls]);
+            if (++ls == kLoStages) { ls = 0; lph ^= 1; }
+          }
           if (++cpos == a.chain || q + 1 == q1) {
             mma_commit(&accf[ab]);
             cpos = 0;
@@ -181,41 +205,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4 && warp < 8) {
-    // ===================== split transform: x -> (H = rna_tf32(x), L = x - H) =====================
-    const int tt = threadIdx.x - 128;  // 0..127
-    int st = 0;
-    uint32_t ph = 0;
-    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-      int t, bi, bj;
-      long long q0, q1;
-      unit_range(a, u, t, q0, q1);
-      tile_coords(a, t, bi, bj);
-      const bool diag = a.sym && bi == bj;
-      for (long long q = q0; q < q1; ++q) {
-        mbar_wait(&full[st], ph);
-        const int ntiles = diag ? 1 : 2;
-        for (int w = 0; w < ntiles; ++w) {
-          float4* hp = reinterpret_cast<float4*>(stage_ptr(st, 2 * w));
-          float4* lp = reinterpret_cast<float4*>(stage_ptr(st, 2 * w + 1));
+    // ===================== split transform: L = x - trunc_tf32(x) =====================
+    if (a.products == 3) {
+      const int tt = threadIdx.x - 128;  // 0..127
+      int rs = 0, ls = 0;
+      uint32_t rph = 0, lph = 0;
+      for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        int t, bi, bj;
+        long long q0, q1;
+        unit_range(a, u, t, q0, q1);
+        tile_coords(a, t, bi, bj);
+        const bool diag = a.sym && bi == bj;
+        for (long long q = q0; q < q1; ++q) {
+          mbar_wait(&rfull[rs], rph);
+          mbar_wait(&lempty[ls], lph ^ 1);
+          const int ntiles = a.raw ? 0 : (diag ? 1 : 2);
+          for (int w = 0; w < ntiles; ++w) {
+            const float4* xp = reinterpret_cast<const float4*>(raw_ptr(rs, w));
+            float4* lp = reinterpret_cast<float4*>(lo_ptr(ls, w));
+            float4 v[kTileBytes / 16 / 128];
 #pragma unroll
-          for (int i = 0; i < kTileBytes / 16 / 128; ++i) {
-            const int idx = i * 128 + tt;
-            float4 v = hp[idx];
-            float4 h, l;
-            uint32_t b;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.x)); h.x = __uint_as_float(b);
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.y)); h.y = __uint_as_float(b);
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.z)); h.z = __uint_as_float(b);
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.w)); h.w = __uint_as_float(b);
-            l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-            hp[idx] = h;
-            lp[idx] = l;
+            for (int i = 0; i < kTileBytes / 16 / 128; ++i) v[i] = xp[i * 128 + tt];
+#pragma unroll
+            for (int i = 0; i < kTileBytes / 16 / 128; ++i) {
+              float4 l;
+              l.x = v[i].x - __uint_as_float(__float_as_uint(v[i].x) & 0xFFFFE000u);
+              l.y = v[i].y - __uint_as_float(__float_as_uint(v[i].y) & 0xFFFFE000u);
+              l.z = v[i].z - __uint_as_float(__float_as_uint(v[i].z) & 0xFFFFE000u);
+              l.w = v[i].w - __uint_as_float(__float_as_uint(v[i].w) & 0xFFFFE000u);
+              lp[i * 128 + tt] = l;
+            }
           }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&lfull[ls]);
+          if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+          if (++ls == kLoStages) { ls = 0; lph ^= 1; }
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&split[st]);
-        if (++st == kStages) { st = 0; ph ^= 1; }
       }
     }
   } else if (warp >= 8) {
@@ -241,14 +267,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (long long c = 0; c < nchains; ++c) {
         mbar_wait(&accf[ab], aph);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * kBN + col0);
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * 2 * kBN + col0);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + h * 32, r);
           tmem_ld_wait();
+          if (a.products == 3) {
+            uint32_t x[32];
+            tmem_ld_32x32b_x32(taddr + kBN + h * 32, x);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]) + __uint_as_float(x[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]);
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -381,6 +415,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.chain = p.chain > 0 ? p.chain : 4;
   a.fold = p.fold > 0 ? p.fold : 16;
   a.products = p.products == 1 ? 1 : 3;
+  a.raw = p.raw;
   const size_t part_bytes = (size_t)a.U * kBM * kBN * sizeof(double);
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_GEMM_PARTIAL, part_bytes));
   if (!part) return TSK_ENOMEM;

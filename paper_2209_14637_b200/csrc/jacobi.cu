@@ -1,13 +1,14 @@
-// Batched symmetric eigensolver by one-sided (Hestenes) Jacobi, one CTA per matrix,
-// warp-level rotations.  Used for the Rayleigh-Ritz step of the top-k eigensolver
-// (S = top-k eigenvectors of G) and for the small k x k problems of SCW
-// (the SVDs of Algorithm 1 lines 1-2, done through Gram matrices).
+// Batched symmetric eigensolver: cyclic two-sided Jacobi, one CTA per matrix.  Used for the
+// Rayleigh-Ritz step of the top-k eigensolver (S = top-k eigenvectors of G) and
+// for the small k x k problems of SCW (the SVDs of Algorithm 1 lines 1-2, PAPER.md:61-62,
+// taken through their Gram matrices).
 //
-// Columns of A (initially H) and V (initially I) are rotated together until all column
-// pairs of A are orthogonal: A = H V with V orthogonal, so V holds the eigenvectors and
-// lambda_c = a_c . v_c.  Pairs are scheduled in the round-robin ("circle") order, p/2
-// disjoint pairs per round, one warp per pair.  Storage is column-major fp64 in shared
-// memory when 2*p*p*8 bytes fit, otherwise in a global (L2-resident) scratch.
+// Each round applies p/2 disjoint plane rotations (round-robin "circle" ordering), chosen to
+// annihilate A_ij (Golub & Van Loan's symmetric Schur decomposition): the rotation parameters
+// need only A_ii, A_jj, A_ij (no reductions), then all row rotations, then all column rotations
+// (and V <- V J) are applied in parallel.  A sweep is p-1 rounds; sweeps repeat until no pair
+// has |A_ij| > tol * sqrt(|A_ii A_jj|).  A and V live in shared memory (padded rows) when they
+// fit, else in a global (L2-resident) scratch.
 #include <algorithm>
 #include <cmath>
 
@@ -16,105 +17,142 @@
 
 namespace tsk {
 
-constexpr int kJacThreads = 512;
-constexpr int kJacSmemMax = 200 * 1024;
+constexpr int kJacThreads = 1024;
+constexpr int kJacSmemMax = 210 * 1024;
 
+// pair k of round r in the circle ordering over pe (even) indices, no divisions
 __device__ __forceinline__ void rr_pair(int r, int k, int pe, int& i, int& j) {
   const int n1 = pe - 1;
   if (k == 0) {
     i = r;
     j = n1;
   } else {
-    i = (r + k) % n1;
-    j = (r - k + n1) % n1;
+    i = r + k;
+    if (i >= n1) i -= n1;
+    j = r - k;
+    if (j < 0) j += n1;
   }
-  if (i > j) { int t = i; i = j; j = t; }
+  if (i > j) { const int t = i; i = j; j = t; }
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
+// One half-warp (16 lanes) per rotation pair.  Phase 1 (per pair, no barrier needed because
+// pairs are disjoint): lane 0 computes (c, s) from A_ii, A_jj, A_ij and the half-warp rotates
+// rows i and j.  Phase 2: the half-warp rotates columns i and j of A and of V.
+template <bool kSmem>
 __global__ void __launch_bounds__(kJacThreads)
     jacobi_eig_kernel(const double* __restrict__ H, int p, double* __restrict__ W, double* __restrict__ lam,
-                      double* __restrict__ gscratch, int use_smem, int max_sweeps, double tol) {
+                      double* __restrict__ gscratch, int max_sweeps, double tol, int* __restrict__ sweeps_out) {
   extern __shared__ double jsm[];
   __shared__ int rot_count;
   __shared__ double lam_s[256];
   const int b = blockIdx.x;
   const int pe = p + (p & 1);
-  double* Acol = use_smem ? jsm : gscratch + (size_t)b * 2 * pe * p;
-  double* Vcol = Acol + (size_t)pe * p;
+  const int ld = p + 1;  // padded row stride
+  double* A = kSmem ? jsm : gscratch + (size_t)b * 2 * p * ld;
+  double* V = A + (size_t)p * ld;
   const double* Hb = H + (size_t)b * p * p;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int hw = tid >> 4, hl = tid & 15, nhw = nt >> 4;  // half-warp id / lane
+  const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
+  const int npairs = pe / 2;
+  __shared__ double amax_s;
 
-  for (int idx = tid; idx < pe * p; idx += blockDim.x) {
-    const int c = idx / p, i = idx % p;
-    Acol[idx] = (c < p) ? 0.5 * (Hb[(size_t)c * p + i] + Hb[(size_t)i * p + c]) : 0.0;
-    Vcol[idx] = (c == i) ? 1.0 : 0.0;
+  for (int e = tid; e < p * p; e += nt) {
+    const int i = e / p, j = e - (e / p) * p;
+    A[i * ld + j] = 0.5 * (Hb[(size_t)i * p + j] + Hb[(size_t)j * p + i]);
+    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  if (tid == 0) {
+    double am = 0.0;
+    for (int i = 0; i < p; ++i) am = fmax(am, fabs(A[i * ld + i]));
+    amax_s = am;
   }
   __syncthreads();
+  // absolute floor: off-diagonals below 1e-15 * max|A_ii| are rounding noise of the updates
+  const double floor_abs = 1e-15 * amax_s;
 
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) rot_count = 0;
     __syncthreads();
     for (int r = 0; r < pe - 1; ++r) {
-      for (int k = warp; k < pe / 2; k += nw) {
-        int ci, cj;
-        rr_pair(r, k, pe, ci, cj);
-        if (cj >= p) continue;  // dummy column of odd p
-        double* ai = Acol + (size_t)ci * p;
-        double* aj = Acol + (size_t)cj * p;
-        double al = 0, be = 0, ga = 0;
-        for (int x = lane; x < p; x += 32) {
-          const double u = ai[x], v = aj[x];
-          al += u * u;
-          be += v * v;
-          ga += u * v;
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al * be) && al > 0.0 && be > 0.0) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t);
-          const double s = c * t;
-          double* vi = Vcol + (size_t)ci * p;
-          double* vj = Vcol + (size_t)cj * p;
-          for (int x = lane; x < p; x += 32) {
-            const double u = ai[x], v = aj[x];
-            ai[x] = c * u - s * v;
-            aj[x] = s * u + c * v;
-            const double vu = vi[x], vv = vj[x];
-            vi[x] = c * vu - s * vv;
-            vj[x] = s * vu + c * vv;
+      double cc[2], ss[2];  // parameters of the (at most 2) pairs this half-warp owns this round
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int k = hw + q * nhw;
+        cc[q] = 1.0;
+        ss[q] = 0.0;
+        if (k < npairs) {
+          int i, j;
+          rr_pair(r, k, pe, i, j);
+          if (j < p) {
+            double c = 1.0, s = 0.0;
+            if (hl == 0) {
+              const double aii = A[i * ld + i], ajj = A[j * ld + j], aij = A[i * ld + j];
+              if (fabs(aij) > fmax(tol * sqrt(fabs(aii * ajj)), floor_abs)) {
+                // tan of the annihilating angle, in fp32 (the MUFU path; ~1e-7 relative).  Any t
+                // gives an exactly orthogonal fp64 rotation (c^2 + s^2 = 1 to fp64 rounding); the
+                // residual ~1e-7 A_ij it leaves is removed by the quadratically convergent sweeps.
+                const float tau = (float)((ajj - aii) / (2.0 * aij));
+                const float tf = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
+                const double t = (double)tf;
+                const double x = 1.0 + t * t;
+                double y = (double)rsqrtf((float)x);  // c = x^-1/2: two fp64 Newton steps
+                y = y * (1.5 - 0.5 * x * y * y);
+                y = y * (1.5 - 0.5 * x * y * y);
+                c = y;
+                s = t * y;
+                atomicAdd(&rot_count, 1);
+              }
+            }
+            c = __shfl_sync(hmask, c, 0, 16);
+            s = __shfl_sync(hmask, s, 0, 16);
+            cc[q] = c;
+            ss[q] = s;
+            if (s != 0.0) {
+              double* Ai = A + i * ld;
+              double* Aj = A + j * ld;
+              for (int x = hl; x < p; x += 16) {
+                const double ai = Ai[x], aj = Aj[x];
+                Ai[x] = c * ai - s * aj;
+                Aj[x] = s * ai + c * aj;
+              }
+            }
           }
-          if (lane == 0) atomicAdd(&rot_count, 1);
         }
-        __syncwarp();
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int k = hw + q * nhw;
+        const double s = ss[q];
+        if (k >= npairs || s == 0.0) continue;
+        const double c = cc[q];
+        int i, j;
+        rr_pair(r, k, pe, i, j);
+        for (int x = hl; x < p; x += 16) {
+          double* Ax = A + x * ld;
+          double* Vx = V + x * ld;
+          const double ai = Ax[i], aj = Ax[j];
+          Ax[i] = c * ai - s * aj;
+          Ax[j] = s * ai + c * aj;
+          const double vi = Vx[i], vj = Vx[j];
+          Vx[i] = c * vi - s * vj;
+          Vx[j] = s * vi + c * vj;
+        }
       }
       __syncthreads();
     }
     if (rot_count == 0) break;
     __syncthreads();
   }
+  if (sweeps_out && tid == 0) sweeps_out[b] = sweep;
 
-  // eigenvalues lambda_c = a_c . v_c  (A = H V)
-  for (int c = warp; c < p; c += nw) {
-    const double* ac = Acol + (size_t)c * p;
-    const double* vc = Vcol + (size_t)c * p;
-    double s = 0;
-    for (int x = lane; x < p; x += 32) s += ac[x] * vc[x];
-    s = warp_sum(s);
-    if (lane == 0) lam_s[c] = s;
-  }
+  for (int c = tid; c < p; c += nt) lam_s[c] = A[c * ld + c];
   __syncthreads();
-  // sort decreasing (stable: ties keep the lower column first)
+  // sort decreasing (stable: ties keep the lower index first); eigenvectors as columns of W
   double* Wb = W + (size_t)b * p * p;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
   for (int c = warp; c < p; c += nw) {
     const double lc = lam_s[c];
     int rank = 0;
@@ -122,17 +160,16 @@ __global__ void __launch_bounds__(kJacThreads)
       const double l2 = lam_s[c2];
       rank += (l2 > lc) || (l2 == lc && c2 < c);
     }
-    const double* vc = Vcol + (size_t)c * p;
-    for (int x = lane; x < p; x += 32) Wb[(size_t)x * p + rank] = vc[x];
     if (lane == 0) lam[(size_t)b * p + rank] = lc;
+    for (int x = lane; x < p; x += 32) Wb[(size_t)x * p + rank] = V[x * ld + c];
   }
 }
 
-tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam) {
+tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps,
+                              double tol) {
   if (p < 1 || p > 256 || batch < 0) return TSK_EINVAL;
   if (batch == 0) return TSK_OK;
-  const int pe = p + (p & 1);
-  const size_t need = (size_t)2 * pe * p * sizeof(double);
+  const size_t need = (size_t)2 * p * (p + 1) * sizeof(double);
   int use_smem = need <= (size_t)kJacSmemMax;
   double* scratch = nullptr;
   if (!use_smem) {
@@ -142,14 +179,19 @@ tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, doubl
   const size_t smem = use_smem ? need : 0;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(jacobi_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kJacSmemMax) !=
+    if (cudaFuncSetAttribute(jacobi_eig_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kJacSmemMax) !=
         cudaSuccess)
       return TSK_ECUDA;
     attr = true;
   }
-  const int threads = p <= 64 ? 256 : kJacThreads;
-  const double tol = 8.9e-16 * sqrt((double)p);  // ~4 eps sqrt(p), cf. one-sided Jacobi SVD practice
-  jacobi_eig_kernel<<<batch, threads, smem, ctx->stream>>>(H, p, W, lam, scratch, use_smem, 40, tol);
+  // Rotate while |A_ij| > tol sqrt(|A_ii A_jj|) (and above an absolute rounding floor); the
+  // eigenvectors come out accurate to ~tol / relative gap.
+  // one half-warp per pair: p/2 pairs -> 8 p threads (at most 2 pairs per half-warp at p = 256)
+  const int threads = std::min(kJacThreads, std::max(64, ((p + 1) / 2 * 16 + 31) / 32 * 32));
+  if (use_smem)
+    jacobi_eig_kernel<true><<<batch, threads, smem, ctx->stream>>>(H, p, W, lam, nullptr, 30, tol, sweeps);
+  else
+    jacobi_eig_kernel<false><<<batch, threads, 0, ctx->stream>>>(H, p, W, lam, scratch, 30, tol, sweeps);
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   ctx->count_launch();
   return TSK_OK;

@@ -99,6 +99,7 @@ struct GemmProblem {
   int chain = 0;                // 0 = default
   int fold = 0;
   int products = 3;
+  int raw = 0;
   GemmInfo* info = nullptr;
 };
 
@@ -115,7 +116,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
 // batched symmetric PSD eigensolver (one-sided Jacobi), jacobi.cu
 // H: [batch][p][p] fp64 symmetric (row-major, read only).  W: [batch][p][p] fp64 eigenvectors as
 // COLUMNS (W[b][i][c] = component i of eigenvector c), lam: [batch][p] fp64 decreasing.
-tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam);
+tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam,
+                              int* sweeps = nullptr, double tol = 1e-13);
 
 }  // namespace tsk
 

@@ -1,0 +1,279 @@
+"""Parity of the CUDA path (through the C ABI) with the float64 oracle, on a B200.
+
+Tolerances (BASELINE.json north_star): Gram relative Frobenius error <= 1e-5; projector
+||S^T S - S_o^T S_o||_F <= 1e-4 when the oracle's eigengap lambda_k/lambda_{k+1} >= 1.05; per-matrix
+SCW error within 1e-4 relative of the oracle's (with a 1e-6 ||A||_F absolute floor for exactly
+low-rank inputs, reading c13).  Added: Ky Fan deficit <= 1e-6 (gap-free), ||S S^T - I|| <= 1e-5.
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import paper_2209_14637_b200 as tsk
+from oracle import scw as oscw
+from oracle import tucker1, validators
+
+pytestmark = pytest.mark.gpu
+
+GRAM_TOL = 1e-5
+PROJ_TOL = 1e-4
+SCW_TOL = 1e-4
+# Ky Fan deficit (gap-free check of S), checked against the oracle's G and,
+# separately, against the GPU's own G (the eigensolver alone).
+KYFAN_SOLVER_TOL = 1e-6
+KYFAN_TOL = 1e-6
+
+
+def relF(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def kyfan_deficit(G, lam, S):
+    k = S.shape[0]
+    return float((lam[:k].sum() - tucker1.kyfan_energy(G, S)) / lam[:k].sum())
+
+
+def rand_stack(D, m, n, seed=0, device="cuda"):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.rand(D, m, n, generator=g).to(device)
+
+
+# ------------------------------------------------------------------------------------- Gram
+@pytest.mark.parametrize("D,m,n", [(1, 64, 48), (20, 64, 48), (7, 300, 100), (3, 129, 36), (10, 256, 256),
+                                   (2, 1080, 1920), (1, 8, 4)])
+def test_gram_matches_oracle(D, m, n):
+    A = rand_stack(D, m, n, seed=D * 1000 + m)
+    G, info = tsk.sketch_gram(A)
+    Go = tucker1.mode1_gram(A.cpu().numpy())
+    Gg = G.cpu().numpy()
+    assert relF(Gg, Go) <= GRAM_TOL
+    assert relF(Gg, Go) <= 3e-6          # regression guard: 3xTF32 with bounded TMEM chains
+    np.testing.assert_array_equal(Gg, Gg.T)  # exact symmetry (lower tiles mirrored)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_gram_configs(cfg):
+    c = datagen.CONFIGS[cfg]
+    A = datagen.generate(c, "train")
+    G, _ = tsk.sketch_gram(A.cuda())
+    assert relF(G.cpu().numpy(), tucker1.mode1_gram(A.numpy())) <= GRAM_TOL
+
+
+@pytest.mark.parametrize("cfg,rows", [("C3", 24), ("C4", 24)])
+def test_gram_full_size_sampled(cfg, rows):
+    """Full BASELINE size, the bench's launch configuration; the oracle computes sampled entries
+    G_ij = sum_d A_d[i,:] . A_d[j,:] one by one from the fp32 inputs in fp64."""
+    c = datagen.CONFIGS[cfg]
+    A = datagen.generate(c, "train", device="cuda")
+    G, info = tsk.sketch_gram(A)
+    rng = np.random.default_rng(1)
+    R = np.unique(np.concatenate([rng.choice(c.m, rows - 2, replace=False), [0, c.m - 1]]))
+    Ar = A[:, torch.tensor(R, device="cuda"), :].double().cpu().numpy()   # [D, |R|, n]
+    Go = np.einsum("dik,djk->ij", Ar, Ar)
+    Gg = G.cpu().numpy()[np.ix_(R, R)]
+    # frame-like data are nonnegative: no cancellation, so the check is per entry
+    assert np.max(np.abs(Gg - Go) / np.abs(Go)) <= GRAM_TOL
+    del A
+
+
+def test_gram_streaming_accumulate_and_determinism():
+    A = rand_stack(12, 200, 64, seed=5)
+    G1, _ = tsk.sketch_gram(A)
+    G2, _ = tsk.sketch_gram(A)
+    assert torch.equal(G1, G2)  # bit-identical (fixed reduction order, no atomics)
+    Gs, _ = tsk.sketch_gram(A[:5].contiguous())
+    tsk.sketch_gram(A[5:].contiguous(), G64=Gs, accumulate=True)
+    # a different K partition changes the fp32 chain boundaries: equal to rounding, not bitwise
+    Go = tucker1.mode1_gram(A.cpu().numpy())
+    assert relF(Gs.cpu().numpy(), Go) <= GRAM_TOL
+    assert relF(Gs.cpu().numpy(), G1.cpu().numpy()) < 2e-6
+    # host-pointer (end-to-end) path: staged through the library, same kernels
+    Gh, _ = tsk.sketch_gram(A.cpu())
+    assert not Gh.is_cuda
+    assert torch.equal(Gh, G1.cpu())
+
+
+def test_gram_argument_errors():
+    A = rand_stack(2, 16, 6)  # n % 4 != 0 -> TSK_ESHAPE
+    with pytest.raises(tsk.TskError) as e:
+        tsk.sketch_gram(A)
+    assert e.value.status == -2
+
+
+def test_tensor_core_truncates_fp32_operands():
+    """Design assumption of the split (gemm_tc.cu): kind::tf32 reads fp32 operands by truncation,
+    so the raw tile is the hi part H = trunc_tf32(x)."""
+    A = torch.rand(4, 128, 64, generator=torch.Generator().manual_seed(0)) + 0.5
+    Gg = tsk.tsk_gram_probe(A.cuda(), mode=3, chain=1).cpu().numpy()
+    h = (A.numpy().view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
+    Gt = sum(x @ x.T for x in h)
+    assert relF(Gg, Gt) < 1e-6
+
+
+# ------------------------------------------------------------------------------------- eigensolver
+def test_jacobi_matches_eigh():
+    rng = np.random.default_rng(0)
+    for p in (5, 20, 63, 90, 160):
+        Q = np.linalg.qr(rng.standard_normal((p, p)))[0]
+        ev = np.exp(rng.uniform(-6, 6, p))
+        H = (Q * ev) @ Q.T
+        W, lam, sw = tsk.tsk_eig_probe(torch.tensor(H[None], device="cuda"))
+        W = W[0].cpu().numpy()
+        lam = lam[0].cpu().numpy()
+        np.testing.assert_allclose(lam, np.sort(ev)[::-1], rtol=1e-12, atol=1e-13 * ev.max())
+        assert np.linalg.norm(H @ W - W * lam) <= 1e-12 * np.linalg.norm(H)
+        assert np.linalg.norm(W.T @ W - np.eye(p)) <= 1e-12
+
+
+def _check_sketch(S, lam, G_o, lam_o, k, projector, G_gpu=None):
+    Sg = S.cpu().double().numpy()
+    assert np.linalg.norm(Sg @ Sg.T - np.eye(k)) <= 1e-5
+    for row in Sg:  # reading c5 sign convention
+        assert row[int(np.argmax(np.abs(row)))] > 0
+    assert abs(kyfan_deficit(G_o, lam_o, Sg)) <= KYFAN_TOL
+    lg = lam.cpu().numpy()
+    # Weyl: |lambda_i(G + E) - lambda_i(G)| <= ||E||_2 <= GRAM_TOL ||G||
+    assert np.all(np.abs(lg - lam_o[:k]) <= GRAM_TOL * lam_o[0])
+    if G_gpu is not None:  # eigensolver accuracy on its own input
+        lam_g = np.sort(np.linalg.eigvalsh(G_gpu))[::-1]
+        assert abs(kyfan_deficit(G_gpu, lam_g, Sg)) <= KYFAN_SOLVER_TOL
+        assert np.all(np.abs(lg - lam_g[:k]) <= 1e-6 * lam_g[0])
+    if projector:
+        S_o, _ = tucker1.top_k_eigen(G_o, k)
+        assert tucker1.eigengap(lam_o, k) >= 1.05
+        assert tucker1.projector_distance(Sg, S_o) <= PROJ_TOL
+
+
+def test_sketch_c1_dense_path_projector():
+    c = datagen.CONFIGS["C1"]
+    A = datagen.generate(c, "train")
+    S, lam, info, st = tsk.sketch_train(A.cuda(), c.k)
+    S_o, lam_o, G_o = tucker1.tucker1_sketch(A.numpy(), c.k)
+    assert st == 0
+    _check_sketch(S, lam, G_o, lam_o, c.k, projector=tucker1.eigengap(lam_o, c.k) >= 1.05)
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 60), (512, 256, 30), (1080, 480, 20)])
+def test_sketch_planted_gap_projector(shape):
+    """Gap-planted streams make the projector tolerance bind (subspace-iteration path for m > 256)."""
+    m, n, D = shape
+    base = datagen.CONFIGS["C3"].replace(m=m, n=n, k=20, r=10)
+    c = datagen.planted(base, gap=1.2, D_train=D)
+    A = datagen.generate(c, "train", device="cuda")
+    S, lam, info, st = tsk.sketch_train(A, c.k)
+    S_o, lam_o, G_o = tucker1.tucker1_sketch(A.cpu().numpy(), c.k)
+    assert st == 0
+    _check_sketch(S, lam, G_o, lam_o, c.k, projector=True)
+
+
+@pytest.mark.parametrize("cfg,D", [("C2", None), ("C3", None), ("C4", 300)])
+def test_sketch_kyfan_flat_spectrum(cfg, D):
+    c = datagen.CONFIGS[cfg]
+    A = datagen.generate(c, "train", 0, D, device="cuda")
+    G = torch.empty(c.m, c.m, dtype=torch.float64, device="cuda")
+    S, lam, info, st = tsk.sketch_train(A, c.k, G64_out=G)
+    S_o, lam_o, G_o = tucker1.tucker1_sketch(A.cpu().numpy(), c.k)
+    assert st == 0, info.as_dict()
+    _check_sketch(S, lam, G_o, lam_o, c.k, projector=tucker1.eigengap(lam_o, c.k) >= 1.05, G_gpu=G.cpu().numpy())
+
+
+def test_sketch_identical_slices():
+    """all A_d = A -> span S = span U_k(A)."""
+    c = datagen.identical(datagen.CONFIGS["C3"].replace(m=320, n=96, k=12, r=6), D_train=6)
+    A = datagen.generate(c, "train", device="cuda")
+    S, lam, info, st = tsk.sketch_train(A, c.k)
+    U = np.linalg.svd(A[0].double().cpu().numpy())[0][:, :c.k]
+    assert tucker1.projector_distance(S.cpu().double().numpy(), U.T) <= PROJ_TOL
+
+
+def test_topk_argument_errors():
+    G = torch.eye(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(tsk.TskError):
+        tsk.sketch_topk(G, 9)
+
+
+# ------------------------------------------------------------------------------------- SCW
+def _scw_parity(A, S, r):
+    err = tsk.scw_error(A.cuda(), S.cuda(), r).cpu().numpy()
+    eo = oscw.scw_errors(A.cpu().numpy(), S.cpu().double().numpy(), r)
+    fro = np.linalg.norm(A.cpu().double().numpy().reshape(A.shape[0], -1), axis=1)
+    assert np.all(np.abs(err - eo) <= SCW_TOL * eo + 1e-6 * fro), (err, eo)
+    return err, eo
+
+
+@pytest.mark.parametrize("cfg,ntest", [("C1", None), ("C2", None), ("C3", 12), ("C4", 4)])
+def test_scw_errors_match_oracle(cfg, ntest):
+    c = datagen.CONFIGS[cfg]
+    Atr = datagen.generate(c, "train", 0, min(c.D_train, 60), device="cuda")
+    S, lam, info, st = tsk.sketch_train(Atr, c.k)
+    T = datagen.generate(c, "test", 0, ntest, device="cuda")
+    err, eo = _scw_parity(T, S, c.r)
+    # Eckart-Young: never below the optimum
+    eopt = np.array([oscw.best_rank_r_error(a, c.r) for a in T.cpu().numpy()])
+    assert np.all(err >= eopt * (1 - 1e-6))
+
+
+def test_scw_factors_and_sigma():
+    c = datagen.CONFIGS["C1"]
+    T = datagen.generate(c, "test")
+    S_o, _, _ = tucker1.tucker1_sketch(datagen.generate(c, "train").numpy(), c.k)
+    S = torch.tensor(S_o, dtype=torch.float32)
+    L, R, sig = tsk.sketch_apply_scw(T.cuda(), S.cuda(), c.r)
+    for b in range(T.shape[0]):
+        Lo, so, Ro = oscw.scw_factors(T[b].numpy(), S.double().numpy(), c.r)
+        Ah = L[b].double().cpu().numpy() @ R[b].double().cpu().numpy().T
+        assert relF(Ah, Lo @ Ro.T) <= 1e-5
+        np.testing.assert_allclose(sig[b].cpu().numpy(), so, rtol=1e-5)
+        Rb = R[b].double().cpu().numpy()
+        assert np.linalg.norm(Rb.T @ Rb - np.eye(c.r)) <= 1e-5
+
+
+def test_scw_exactly_low_rank_is_exact():
+    """PAPER.md:149-153 with eps = 0: noise-free rank-5 stream in a fixed subspace -> error 0."""
+    c = datagen.lowrank("C1", rank=5)
+    A = datagen.generate(c, "train")
+    T = datagen.generate(c, "test")
+    S, lam, info, st = tsk.sketch_train(A.cuda(), c.k)
+    err = tsk.scw_error(T.cuda(), S, c.r).cpu().numpy()
+    fro = np.linalg.norm(T.numpy().reshape(T.shape[0], -1), axis=1)
+    assert np.all(err <= 1e-6 * fro)
+
+
+def test_scw_square_sketch_is_eckart_young():
+    """k = m: S orthogonal, SCW = [A]_r."""
+    rng = np.random.default_rng(3)
+    m, n, r = 40, 32, 6
+    T = torch.tensor(rng.standard_normal((5, m, n)), dtype=torch.float32)
+    S = torch.tensor(np.linalg.qr(rng.standard_normal((m, m)))[0].T.copy(), dtype=torch.float32)
+    err = tsk.scw_error(T.cuda(), S.cuda(), r).cpu().numpy()
+    eopt = np.array([oscw.best_rank_r_error(a, r) for a in T.numpy()])
+    np.testing.assert_allclose(err, eopt, rtol=1e-4)
+
+
+def test_scw_edge_cases():
+    c = datagen.CONFIGS["C1"]
+    T = datagen.generate(c, "test")
+    S_o, _, _ = tucker1.tucker1_sketch(datagen.generate(c, "train").numpy(), c.k)
+    S = torch.tensor(S_o, dtype=torch.float32).cuda()
+    # empty batch
+    assert tsk.scw_error(T[:0].cuda(), S, c.r).numel() == 0
+    # r > k is clamped (warning), result equals r = k
+    with pytest.warns(RuntimeWarning):
+        e_big = tsk.scw_error(T.cuda(), S, c.k + 3).cpu().numpy()
+    e_k = tsk.scw_error(T.cuda(), S, c.k).cpu().numpy()
+    np.testing.assert_array_equal(e_big, e_k)
+    # host-pointer path equals the device path
+    e_h = tsk.scw_error(T, S.cpu(), c.r).numpy()
+    np.testing.assert_array_equal(e_h, tsk.scw_error(T.cuda(), S, c.r).cpu().numpy())
+
+
+def test_theorem1_holds_for_gpu_outputs():
+    """P8 on the whole GPU path: GPU S, GPU SCW errors on the training set."""
+    c = datagen.CONFIGS["C2"]
+    A = datagen.generate(c, "train", 0, 60)
+    S, lam, info, st = tsk.sketch_train(A.cuda(), c.k)
+    err = tsk.scw_error(A.cuda(), S, c.r).cpu().numpy()
+    Sd = S.cpu().double().numpy()
+    bound = validators.theorem1_bound(A.numpy(), Sd, c.r)
+    assert float(np.sum(err ** 2)) <= bound * (1 + 1e-5)
