@@ -127,6 +127,7 @@ tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const
    same contract as sketch_gram (device pointers only, accumulate = 0) with
      mode bit 0: skip the in-shared-memory hi/lo split (the MMA consumes the raw fp32 tiles),
      mode bit 1: issue only the H*H^T product (1xTF32),
+     mode bit 2: disable the drift throttle between units sharing a K window,
    chain / splits as in tsk_train_opts (0 = default). */
 tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int mode, int chain,
                           int splits);

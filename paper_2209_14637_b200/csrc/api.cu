@@ -454,6 +454,7 @@ tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, 
   p.splits = splits;
   p.raw = mode & 1;
   p.products = (mode & 2) ? 1 : 3;
+  p.lag = (mode & 4) ? 0 : -1;
   return tsk::gemm_tf32x3(&ctx->c, p);
 }
 

@@ -52,7 +52,9 @@ struct GemmArgs {
   int fold;      // chains per fp64 fold
   int products;  // 3 = split-TF32 (production); 1 = H*H only (precision probe)
   int raw;       // diagnostics: 1 = skip the split transform (the lo buffers are not written)
+  int lag;       // drift throttle: max chunks a unit may run ahead of its K-split peers (0 = off)
   double* part;  // [U][128][128] fp64 partials
+  unsigned* progress;  // [U] chunks issued per unit (drift throttle)
 };
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& bi, int& bj) {
@@ -130,25 +132,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto lo_ptr = [&](int st, int which) { return lo_base + (st * 2 + which) * kTileBytes; };
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (elect_one()) {
-      int st = 0;
-      uint32_t ph = 0;
-      for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-        int t, bi, bj;
-        long long q0, q1;
-        unit_range(a, u, t, q0, q1);
-        tile_coords(a, t, bi, bj);
-        const bool diag = a.sym && bi == bj;
-        for (long long q = q0; q < q1; ++q) {
+    // ===================== TMA producer (lane 0 issues; the warp runs the drift throttle) =====================
+    // Units of the same K-split s in the same round read the same K window; if they drift apart
+    // the window leaves L2 and every tile re-reads its rows from HBM (measured 6x over-read).
+    // Every 32 chunks each unit publishes its progress and waits while it is more than `lag`
+    // chunks ahead of the slowest such peer (the slowest never waits: no deadlock).
+    int st = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      int t, bi, bj;
+      long long q0, q1;
+      unit_range(a, u, t, q0, q1);
+      tile_coords(a, t, bi, bj);
+      const bool diag = a.sym && bi == bj;
+      const int s_split = u / a.T;
+      const int round = u / gridDim.x;
+      for (long long q = q0; q < q1; ++q) {
+        if (lane == 0) {
           mbar_wait(&rempty[st], ph ^ 1);
           mbar_arrive_expect_tx(&rfull[st], diag ? kTileBytes : 2 * kTileBytes);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
           tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
           if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * kBN, z);
-          if (++st == kRawStages) { st = 0; ph ^= 1; }
         }
+        if (++st == kRawStages) { st = 0; ph ^= 1; }
+        const unsigned done = (unsigned)(q - q0 + 1);
+        if (a.lag > 0 && ((done & 31u) == 0 || q + 1 == q1)) {
+          if (lane == 0) st_volatile_u32(&a.progress[u], q + 1 == q1 ? 0xFFFFFFFFu : done);
+          if (q + 1 < q1) {
+            while (true) {
+              unsigned mn = 0xFFFFFFFFu;
+              for (int tp = lane; tp < a.T; tp += 32) {
+                const int up = s_split * a.T + tp;
+                if (up != u && up / (int)gridDim.x == round) mn = min(mn, ld_volatile_u32(&a.progress[up]));
+              }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+              if (mn == 0xFFFFFFFFu || done <= mn + (unsigned)a.lag) break;
+              __nanosleep(1000);
+            }
+          }
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -289,6 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&acce[ab]);
         if (++ab == 2) { ab = 0; aph ^= 1; }
         if (++cin == a.fold || c + 1 == nchains) {
+          // partial-sum lines are re-read every fold: keep them in L2 against the streaming operands
+          const uint64_t pol = l2_policy_evict_last();
 #pragma unroll
           for (int i = 0; i < 64; i += 2) {
             double2* p2 = reinterpret_cast<double2*>(prow + i);
@@ -297,11 +325,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               v.x = (double)sum[i];
               v.y = (double)sum[i + 1];
             } else {
-              v = *p2;
+              v = ld_f64x2_hint(p2, pol);
               v.x += (double)sum[i];
               v.y += (double)sum[i + 1];
             }
-            *p2 = v;
+            st_f64x2_hint(p2, v, pol);
             sum[i] = 0.f;
             sum[i + 1] = 0.f;
           }
@@ -416,10 +444,15 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.fold = p.fold > 0 ? p.fold : 16;
   a.products = p.products == 1 ? 1 : 3;
   a.raw = p.raw;
+  a.lag = p.lag >= 0 ? p.lag : 64;
   const size_t part_bytes = (size_t)a.U * kBM * kBN * sizeof(double);
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_GEMM_PARTIAL, part_bytes));
   if (!part) return TSK_ENOMEM;
   a.part = part;
+  unsigned* prog = reinterpret_cast<unsigned*>(ctx->workspace(WS_GEMM_PROGRESS, (size_t)a.U * sizeof(unsigned)));
+  if (!prog) return TSK_ENOMEM;
+  a.progress = prog;
+  if (cudaMemsetAsync(prog, 0, (size_t)a.U * sizeof(unsigned), ctx->stream) != cudaSuccess) return TSK_ECUDA;
 
   static bool attr_set = false;
   if (!attr_set) {

@@ -29,6 +29,7 @@ enum WorkspaceId {
   WS_SCW_5,
   WS_GRAM,       // fp64 Gram for sketch_train
   WS_JACOBI,
+  WS_GEMM_PROGRESS,
   WS_COUNT
 };
 
@@ -100,6 +101,7 @@ struct GemmProblem {
   int fold = 0;
   int products = 3;
   int raw = 0;
+  int lag = -1;  // drift throttle (chunks); -1 = default, 0 = off
   GemmInfo* info = nullptr;
 };
 
