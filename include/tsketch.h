@@ -128,6 +128,7 @@ tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const
      mode bit 0: skip the in-shared-memory hi/lo split (the MMA consumes the raw fp32 tiles),
      mode bit 1: issue only the H*H^T product (1xTF32),
      mode bit 2: disable the drift throttle between units sharing a K window,
+     mode bit 3: use the SS kernel variant (A operand from shared memory instead of TMEM),
    chain / splits as in tsk_train_opts (0 = default). */
 tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int mode, int chain,
                           int splits);

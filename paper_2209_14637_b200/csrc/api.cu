@@ -455,6 +455,7 @@ tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, 
   p.raw = mode & 1;
   p.products = (mode & 2) ? 1 : 3;
   p.lag = (mode & 4) ? 0 : -1;
+  p.ss = (mode & 8) ? 1 : 0;
   return tsk::gemm_tf32x3(&ctx->c, p);
 }
 

@@ -348,6 +348,279 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// TS variant (production path): the A operand (hi and lo parts of the X rows) is written by the
+// transform warps straight into tensor memory with tcgen05.st, so the MMAs read only their B
+// operand from shared memory.  Per 32-column chunk of an off-diagonal 128x128 tile this moves
+// 128 KB through shared memory (TMA 32 + transform 48 + MMA-B 48) instead of 192 KB.
+// TMEM: two 128-column accumulators (double buffer; H H^T and the cross terms share one) + three
+// 64-column A stages [H_X | L_X].  Shared memory: 5 raw TMA stages [X|Y] + 3 lo stages [L_Y].
+constexpr int kTsLoStages = 3;
+constexpr int kTsSmemBytes = (kRawStages * 2 + kTsLoStages) * kTileBytes + 1024 + 256;
+constexpr uint32_t kTsAccCols = 128;
+constexpr uint32_t kTsAStageCols = 64;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
+                          const GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* raw_base = smem;                                 // [kRawStages][X|Y]
+  uint8_t* lo_base = smem + kRawStages * 2 * kTileBytes;    // [kTsLoStages][L_Y]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lo_base + kTsLoStages * kTileBytes);
+  uint64_t* rfull = bars;
+  uint64_t* rempty = rfull + kRawStages;
+  uint64_t* lfull = rempty + kRawStages;
+  uint64_t* lempty = lfull + kTsLoStages;
+  uint64_t* accf = lempty + kTsLoStages;
+  uint64_t* acce = accf + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mapX);
+    tma_prefetch_desc(&mapY);
+    for (int i = 0; i < kRawStages; ++i) {
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], 1);
+    }
+    for (int i = 0; i < kTsLoStages; ++i) {
+      mbar_init(&lfull[i], 4);
+      mbar_init(&lempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto raw_ptr = [&](int st, int which) { return raw_base + (st * 2 + which) * kTileBytes; };
+  auto lo_ptr = [&](int st) { return lo_base + st * kTileBytes; };
+
+  if (warp == 0) {
+    // ===================== TMA producer + drift throttle (as in the SS kernel) =====================
+    int st = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      int t, bi, bj;
+      long long q0, q1;
+      unit_range(a, u, t, q0, q1);
+      tile_coords(a, t, bi, bj);
+      const bool diag = a.sym && bi == bj;
+      const int s_split = u / a.T;
+      const int round = u / gridDim.x;
+      for (long long q = q0; q < q1; ++q) {
+        if (lane == 0) {
+          mbar_wait(&rempty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&rfull[st], diag ? kTileBytes : 2 * kTileBytes);
+          const int z = (int)(q / a.cps);
+          const int kc = (int)(q % a.cps) * kBK;
+          tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
+          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * kBN, z);
+        }
+        if (++st == kRawStages) { st = 0; ph ^= 1; }
+        const unsigned done = (unsigned)(q - q0 + 1);
+        if (a.lag > 0 && ((done & 31u) == 0 || q + 1 == q1)) {
+          if (lane == 0) st_volatile_u32(&a.progress[u], q + 1 == q1 ? 0xFFFFFFFFu : done);
+          if (q + 1 < q1) {
+            while (true) {
+              unsigned mn = 0xFFFFFFFFu;
+              for (int tp = lane; tp < a.T; tp += 32) {
+                const int up = s_split * a.T + tp;
+                if (up != u && up / (int)gridDim.x == round) mn = min(mn, ld_volatile_u32(&a.progress[up]));
+              }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+              if (mn == 0xFFFFFFFFu || done <= mn + (unsigned)a.lag) break;
+              __nanosleep(1000);
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread) =====================
+    if (elect_one()) {
+      const uint32_t idesc = idesc_tf32(kBM, kBN);
+      int rs = 0, ls = 0;
+      uint32_t rph = 0, lph = 0;
+      int ab = 0;
+      uint32_t aph = 0;
+      for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        int t, bi, bj;
+        long long q0, q1;
+        unit_range(a, u, t, q0, q1);
+        tile_coords(a, t, bi, bj);
+        const bool diag = a.sym && bi == bj;
+        int cpos = 0;
+        for (long long q = q0; q < q1; ++q) {
+          if (cpos == 0) {
+            mbar_wait(&acce[ab], aph ^ 1);
+            tc_fence_after();
+          }
+          mbar_wait(&lfull[ls], lph);  // transform done: implies the raw stage landed
+          tc_fence_after();
+          const uint32_t d = tmem_base + (uint32_t)ab * kTsAccCols;
+          const uint32_t a_hi = tmem_base + 2 * kTsAccCols + (uint32_t)ls * kTsAStageCols;
+          const uint32_t a_lo = a_hi + 32;
+          const uint64_t yh = sw128_kmajor_desc(smem_u32(raw_ptr(rs, diag ? 0 : 1)));
+          const uint64_t yl = sw128_kmajor_desc(smem_u32(lo_ptr(ls)));
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint64_t adv = (uint64_t)(kk * 32 >> 4);  // +32 B per K=8 step inside the swizzle atom
+            mma_tf32_ts(d, a_hi + kk * 8, yh + adv, idesc, (cpos > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32_ts(d, a_hi + kk * 8, yl + adv, idesc, 1u);
+            mma_tf32_ts(d, a_lo + kk * 8, yh + adv, idesc, 1u);
+          }
+          mma_commit(&rempty[rs]);
+          if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+          mma_commit(&lempty[ls]);
+          if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
+          if (++cpos == a.chain || q + 1 == q1) {
+            mma_commit(&accf[ab]);
+            cpos = 0;
+            if (++ab == 2) { ab = 0; aph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ===================== transform: X rows -> TMEM (H, L); Y tile -> L_Y in shared memory ========
+    const int tt = threadIdx.x - 128;  // 0..127 = tile row handled for the TMEM A operand
+    const int quad = warp & 3;         // == tt / 32: the TMEM lane quadrant of this warp
+    int rs = 0, ls = 0;
+    uint32_t rph = 0, lph = 0;
+    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      int t, bi, bj;
+      long long q0, q1;
+      unit_range(a, u, t, q0, q1);
+      tile_coords(a, t, bi, bj);
+      const bool diag = a.sym && bi == bj;
+      for (long long q = q0; q < q1; ++q) {
+        mbar_wait(&rfull[rs], rph);
+        mbar_wait(&lempty[ls], lph ^ 1);
+        tc_fence_after();
+        // (1) row tt of X (128-B swizzled row: 16-B chunk c at position c ^ (tt & 7))
+        {
+          const uint32_t xrow = smem_u32(raw_ptr(rs, 0)) + (uint32_t)tt * 128u;
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = lds_f4(xrow + (uint32_t)((c ^ (tt & 7)) * 16));
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t h = __float_as_uint(e[j]) & 0xFFFFE000u;
+              hi[c * 4 + j] = h;
+              lo[c * 4 + j] = __float_as_uint(e[j] - __uint_as_float(h));
+            }
+          }
+          const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + 2 * kTsAccCols + (uint32_t)ls * kTsAStageCols;
+          tmem_st_32x32b_x32(ta, hi);
+          tmem_st_32x32b_x32(ta + 32, lo);
+        }
+        // (2) the B-side lo part: L_Y (or L_X for a diagonal tile) in the swizzled smem layout
+        {
+          const uint32_t src = smem_u32(raw_ptr(rs, diag ? 0 : 1));
+          const uint32_t dst = smem_u32(lo_ptr(ls));
+#pragma unroll
+          for (int i = 0; i < kTileBytes / 16 / 128; ++i) {
+            const uint32_t off = (uint32_t)(i * 128 + tt) * 16u;
+            const float4 v = lds_f4(src + off);
+            float4 l;
+            l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+            l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+            l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+            l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            sts_f4(dst + off, l);
+          }
+        }
+        tmem_st_wait();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lfull[ls]);
+        if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+        if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ===================== epilogue: TMEM chains -> fp32 registers -> fp64 partials =====================
+    const int e = warp - 8;
+    const int quad = warp & 3;
+    const int col0 = (e >> 2) * 64;
+    const int row = quad * 32 + lane;
+    int ab = 0;
+    uint32_t aph = 0;
+    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      int t;
+      long long q0, q1;
+      unit_range(a, u, t, q0, q1);
+      const long long nchains = (q1 - q0 + a.chain - 1) / a.chain;
+      float sum[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+      int cin = 0;
+      bool first_fold = true;
+      double* prow = a.part + (size_t)u * (kBM * kBN) + (size_t)row * kBN + col0;
+      for (long long c = 0; c < nchains; ++c) {
+        mbar_wait(&accf[ab], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)ab * kTsAccCols + col0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + h * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acce[ab]);
+        if (++ab == 2) { ab = 0; aph ^= 1; }
+        if (++cin == a.fold || c + 1 == nchains) {
+          const uint64_t pol = l2_policy_evict_last();
+#pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            double2* p2 = reinterpret_cast<double2*>(prow + i);
+            double2 v;
+            if (first_fold) {
+              v.x = (double)sum[i];
+              v.y = (double)sum[i + 1];
+            } else {
+              v = ld_f64x2_hint(p2, pol);
+              v.x += (double)sum[i];
+              v.y += (double)sum[i + 1];
+            }
+            st_f64x2_hint(p2, v, pol);
+            sum[i] = 0.f;
+            sum[i + 1] = 0.f;
+          }
+          first_fold = false;
+          cin = 0;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
 // Sum the S partials of every tile in fixed order; write fp64 (and optionally fp32) output.
 // sym: only i >= j is summed and mirrored to (j, i), so the result is exactly symmetric.
 __global__ void gemm_finalize_kernel(const double* __restrict__ part, int M, int N, int T, int nb, int S, int sym,
@@ -457,12 +730,18 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
-        cudaSuccess)
+            cudaSuccess ||
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes) !=
+            cudaSuccess)
       return TSK_ECUDA;
     attr_set = true;
   }
   const int grid = std::min(a.U, ctx->num_sms);
-  gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(mx, my, a);
+  // production: TS variant (A operand from TMEM); the SS variant serves the diagnostic modes
+  if (a.products == 3 && !a.raw && !p.ss)
+    gemm_tf32x3_ts_kernel<<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+  else
+    gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(mx, my, a);
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   ctx->count_launch();
 

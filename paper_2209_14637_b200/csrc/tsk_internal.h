@@ -102,6 +102,7 @@ struct GemmProblem {
   int products = 3;
   int raw = 0;
   int lag = -1;  // drift throttle (chunks); -1 = default, 0 = off
+  int ss = 0;    // 1: force the SS kernel variant (A operand from shared memory)
   GemmInfo* info = nullptr;
 };
 
