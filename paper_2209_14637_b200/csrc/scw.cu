@@ -22,41 +22,6 @@
 
 namespace tsk {
 
-// ---------------------------------------------------------------- 1. B = S A
-template <int KMAX>
-__global__ void __launch_bounds__(128) scw_sa_kernel(const float* __restrict__ A, const float* __restrict__ S, int m,
-                                                     int n, int k, float* __restrict__ Bm) {
-  __shared__ float Ss[KMAX][33];
-  const int b = blockIdx.y;
-  const int j = blockIdx.x * 128 + threadIdx.x;
-  const float* Ab = A + (size_t)b * m * n;
-  float acc[KMAX];
-#pragma unroll
-  for (int c = 0; c < KMAX; ++c) acc[c] = 0.f;
-  for (int i0 = 0; i0 < m; i0 += 32) {
-    for (int e = threadIdx.x; e < KMAX * 32; e += 128) {
-      const int c = e >> 5, ii = e & 31;
-      Ss[c][ii] = (c < k && i0 + ii < m) ? S[(size_t)c * m + i0 + ii] : 0.f;
-    }
-    __syncthreads();
-    if (j < n) {
-      const int lim = min(32, m - i0);
-      for (int ii = 0; ii < lim; ++ii) {
-        const float a = Ab[(size_t)(i0 + ii) * n + j];
-#pragma unroll
-        for (int c = 0; c < KMAX; ++c) acc[c] = fmaf(Ss[c][ii], a, acc[c]);
-      }
-    }
-    __syncthreads();
-  }
-  if (j < n) {
-    float* Bb = Bm + (size_t)b * k * n;
-#pragma unroll
-    for (int c = 0; c < KMAX; ++c)
-      if (c < k) Bb[(size_t)c * n + j] = acc[c];
-  }
-}
-
 // ---------------------------------------------------------------- C = X X^T (rows of an fp32 k x len matrix), fp64
 // grid (ceil(npairs / (256*kPer)), batch); each thread owns kPer lower-triangle pairs (a >= c).
 constexpr int kGramPer = 8;
@@ -118,7 +83,9 @@ static void launch_gram_rows(const float* X, int k, int len, int batch, double* 
 }
 
 // ---------------------------------------------------------------- 2. V^T = diag(mu^-1/2) W^T B
-__global__ void __launch_bounds__(256) scw_vt_kernel(const float* __restrict__ Bm, const double* __restrict__ Wc,
+// thread per column j: its B column (k values) is cached in registers, W comes from shared memory
+template <int KMAX>
+__global__ void __launch_bounds__(128) scw_vt_kernel(const float* __restrict__ Bm, const double* __restrict__ Wc,
                                                      const double* __restrict__ mu, int k, int n,
                                                      float* __restrict__ Vt) {
   extern __shared__ double ws[];  // [k][k] W, then [k] scale
@@ -126,68 +93,31 @@ __global__ void __launch_bounds__(256) scw_vt_kernel(const float* __restrict__ B
   const double* Wb = Wc + (size_t)b * k * k;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) ws[e] = Wb[e];
   double* sc = ws + k * k;
-  if (threadIdx.x < k) {
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
     const double m0 = mu[(size_t)b * k];
-    const double mc = mu[(size_t)b * k + threadIdx.x];
-    sc[threadIdx.x] = (mc > 0.0 && mc > 1e-13 * m0) ? 1.0 / sqrt(mc) : 0.0;
+    const double mc = mu[(size_t)b * k + c];
+    sc[c] = (mc > 0.0 && mc > 1e-13 * m0) ? 1.0 / sqrt(mc) : 0.0;
   }
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const float* Bb = Bm + (size_t)b * k * n;
+  float bv[KMAX];
+#pragma unroll
+  for (int a = 0; a < KMAX; ++a) bv[a] = a < k ? Bb[(size_t)a * n + j] : 0.f;
   float* Vb = Vt + (size_t)b * k * n;
   for (int c = 0; c < k; ++c) {
     double s = 0.0;
-    for (int a = 0; a < k; ++a) s += ws[a * k + c] * (double)Bb[(size_t)a * n + j];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a)
+      if (a < k) s += ws[a * k + c] * (double)bv[a];
     Vb[(size_t)c * n + j] = (float)(s * sc[c]);
   }
 }
 
-// ---------------------------------------------------------------- 3. Z^T = V^T A^T  (k x m)
-template <int KMAX>
-__global__ void __launch_bounds__(256) scw_av_kernel(const float* __restrict__ A, const float* __restrict__ Vt, int m,
-                                                     int n, int k, float* __restrict__ Zt) {
-  __shared__ float As[64][33];
-  __shared__ float Vs[KMAX][33];
-  const int b = blockIdx.y;
-  const int i0 = blockIdx.x * 64;
-  const int r = threadIdx.x & 63, g = threadIdx.x >> 6;
-  const float* Ab = A + (size_t)b * m * n;
-  const float* Vb = Vt + (size_t)b * k * n;
-  constexpr int kOut = KMAX / 4;
-  float acc[kOut];
-#pragma unroll
-  for (int u = 0; u < kOut; ++u) acc[u] = 0.f;
-  for (int j0 = 0; j0 < n; j0 += 32) {
-    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
-      const int ii = e >> 5, jj = e & 31;
-      As[ii][jj] = (i0 + ii < m && j0 + jj < n) ? Ab[(size_t)(i0 + ii) * n + j0 + jj] : 0.f;
-    }
-    for (int e = threadIdx.x; e < KMAX * 32; e += 256) {
-      const int c = e >> 5, jj = e & 31;
-      Vs[c][jj] = (c < k && j0 + jj < n) ? Vb[(size_t)c * n + j0 + jj] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int jj = 0; jj < 32; ++jj) {
-      const float a = As[r][jj];
-#pragma unroll
-      for (int u = 0; u < kOut; ++u) acc[u] = fmaf(Vs[g + 4 * u][jj], a, acc[u]);
-    }
-    __syncthreads();
-  }
-  if (i0 + r < m) {
-    float* Zb = Zt + (size_t)b * k * m;
-#pragma unroll
-    for (int u = 0; u < kOut; ++u) {
-      const int c = g + 4 * u;
-      if (c < k) Zb[(size_t)c * m + i0 + r] = acc[u];
-    }
-  }
-}
-
 // ---------------------------------------------------------------- 5. out[i][c] = sum_a In[a][i] W[a][c], c < r
-__global__ void __launch_bounds__(256) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
+template <int KMAX>
+__global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
                                                           int k, int len, int r, float* __restrict__ Out) {
   extern __shared__ double wsm[];  // [k][r]
   const int b = blockIdx.y;
@@ -197,10 +127,15 @@ __global__ void __launch_bounds__(256) scw_combine_kernel(const float* __restric
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= len) return;
   const float* Ib = In + (size_t)b * k * len;
+  float iv[KMAX];
+#pragma unroll
+  for (int a = 0; a < KMAX; ++a) iv[a] = a < k ? Ib[(size_t)a * len + i] : 0.f;
   float* Ob = Out + (size_t)b * len * r;
   for (int c = 0; c < r; ++c) {
     double s = 0.0;
-    for (int a = 0; a < k; ++a) s += (double)Ib[(size_t)a * len + i] * wsm[a * r + c];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a)
+      if (a < k) s += (double)iv[a] * wsm[a * r + c];
     Ob[(size_t)i * r + c] = (float)s;
   }
 }
@@ -213,60 +148,221 @@ __global__ void scw_sigma_kernel(const double* __restrict__ sig2, int k, int r, 
   sigma[idx] = (float)sqrt(fmax(sig2[b * k + c], 0.0));
 }
 
-// ---------------------------------------------------------------- 6. e^2 partials: sum (A - L R^T)^2
-template <int RMAX>
-__global__ void __launch_bounds__(256) scw_residual_kernel(const float* __restrict__ A, const float* __restrict__ L,
-                                                           const float* __restrict__ R, int m, int n, int r,
-                                                           int rows_per_block, double* __restrict__ part) {
-  __shared__ float Ls[16][RMAX];
-  __shared__ double red[256];
-  const int b = blockIdx.y;
-  const int tile = blockIdx.x;
-  const float* Ab = A + (size_t)b * m * n;
-  const float* Lb = L + (size_t)b * m * r;
-  const float* Rb = R + (size_t)b * n * r;
-  const int i_begin = tile * rows_per_block;
-  const int i_end = min(m, i_begin + rows_per_block);
-  double acc = 0.0;
-  for (int jb = 0; jb < n; jb += 256) {
-    const int j = jb + threadIdx.x;
-    float rr[RMAX];
-#pragma unroll
-    for (int c = 0; c < RMAX; ++c) rr[c] = (j < n && c < r) ? Rb[(size_t)j * r + c] : 0.f;
-    for (int i0 = i_begin; i0 < i_end; i0 += 16) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < 16 * RMAX; e += 256) {
-        const int ii = e / RMAX, c = e % RMAX;
-        Ls[ii][c] = (i0 + ii < i_end && c < r) ? Lb[(size_t)(i0 + ii) * r + c] : 0.f;
-      }
-      __syncthreads();
-      if (j < n) {
-        const int lim = min(16, i_end - i0);
-        for (int ii = 0; ii < lim; ++ii) {
-          float pred = 0.f;
-#pragma unroll
-          for (int c = 0; c < RMAX; ++c) pred = fmaf(Ls[ii][c], rr[c], pred);
-          const double d = (double)Ab[(size_t)(i0 + ii) * n + j] - (double)pred;
-          acc += d * d;
-        }
-      }
-    }
-  }
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[(size_t)b * gridDim.x + tile] = red[0];
-}
-
 __global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles, long long B, double* __restrict__ err) {
   const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   double s = 0.0;
   for (int t = 0; t < tiles; ++t) s += part[b * tiles + t];
   err[b] = sqrt(s);
+}
+
+// ---------------------------------------------------------------- register-tiled SIMT products
+// 256 threads compute a [CB x 128] output tile; thread (ty = tid/16, tx = tid%16) owns rows
+// ty*CT .. ty*CT+CT-1 (CT = CB/16) and columns tx + 16u (u < 8): per contraction step it reads
+// CT + 8 operands from shared memory and issues 8*CT FMAs (fp32, round-to-nearest).
+constexpr int kTK = 16;  // contraction chunk
+
+// Out[b][c][j] = sum_i P[c][i] A[b][i][j]      (B = S A: P = S [k][m], A [m][n], Out [k][n])
+template <int CB>
+__global__ void __launch_bounds__(256) scw_sa_tiled_kernel(const float* __restrict__ A, const float* __restrict__ P,
+                                                           int m, int n, int k, float* __restrict__ Out) {
+  constexpr int CT = CB / 16;
+  __shared__ float Ps[kTK][CB + 4];
+  __shared__ float As[kTK][128 + 4];
+  const int b = blockIdx.z;
+  const int c0 = blockIdx.y * CB, j0 = blockIdx.x * 128;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const float* Ab = A + (size_t)b * m * n;
+  float acc[CT][8];
+#pragma unroll
+  for (int v = 0; v < CT; ++v)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
+  for (int i0 = 0; i0 < m; i0 += kTK) {
+    // A chunk [16][128]: 512 float4, 2 per thread (rows contiguous in j)
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int e = tid + w * 256;
+      const int ii = e >> 5, jq = (e & 31) * 4;
+      const int i = i0 + ii, j = j0 + jq;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < m) {
+        if (j + 3 < n) v = *reinterpret_cast<const float4*>(Ab + (size_t)i * n + j);
+        else {
+          if (j < n) v.x = Ab[(size_t)i * n + j];
+          if (j + 1 < n) v.y = Ab[(size_t)i * n + j + 1];
+          if (j + 2 < n) v.z = Ab[(size_t)i * n + j + 2];
+        }
+      }
+      *reinterpret_cast<float4*>(&As[ii][jq]) = v;
+    }
+    // P chunk [CB][16] -> Ps[16][CB]
+    for (int e = tid; e < CB * kTK; e += 256) {
+      const int c = e >> 4, ii = e & 15;
+      Ps[ii][c] = (c0 + c < k && i0 + ii < m) ? P[(size_t)(c0 + c) * m + i0 + ii] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ii = 0; ii < kTK; ++ii) {
+      float pv[CT], av[8];
+#pragma unroll
+      for (int v = 0; v < CT; ++v) pv[v] = Ps[ii][ty * CT + v];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) av[u] = As[ii][tx + 16 * u];
+#pragma unroll
+      for (int v = 0; v < CT; ++v)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[v][u] = fmaf(pv[v], av[u], acc[v][u]);
+    }
+    __syncthreads();
+  }
+  float* Ob = Out + (size_t)b * k * n;
+#pragma unroll
+  for (int v = 0; v < CT; ++v) {
+    const int c = c0 + ty * CT + v;
+    if (c >= k) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + tx + 16 * u;
+      if (j < n) Ob[(size_t)c * n + j] = acc[v][u];
+    }
+  }
+}
+
+// Out[b][c][i] = sum_j P[b][c][j] A[b][i][j]    (Z^T = V^T A^T: P = V^T [k][n], A [m][n], Out [k][m])
+template <int CB>
+__global__ void __launch_bounds__(256) scw_av_tiled_kernel(const float* __restrict__ A, const float* __restrict__ P,
+                                                           int m, int n, int k, float* __restrict__ Out) {
+  constexpr int CT = CB / 16;
+  __shared__ float Ps[kTK][CB + 4];
+  __shared__ float As[kTK][128 + 4];
+  const int b = blockIdx.z;
+  const int c0 = blockIdx.y * CB, i0 = blockIdx.x * 128;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const float* Ab = A + (size_t)b * m * n;
+  const float* Pb = P + (size_t)b * k * n;
+  float acc[CT][8];
+#pragma unroll
+  for (int v = 0; v < CT; ++v)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
+  for (int j0 = 0; j0 < n; j0 += kTK) {
+    // A chunk rows i0..i0+127, cols j0..j0+15 -> As[jj][i]: 512 float4, 2 per thread
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const int e = tid + w * 256;
+      const int il = e >> 2, jq = (e & 3) * 4;
+      const int i = i0 + il, j = j0 + jq;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < m) {
+        if (j + 3 < n) v = *reinterpret_cast<const float4*>(Ab + (size_t)i * n + j);
+        else {
+          if (j < n) v.x = Ab[(size_t)i * n + j];
+          if (j + 1 < n) v.y = Ab[(size_t)i * n + j + 1];
+          if (j + 2 < n) v.z = Ab[(size_t)i * n + j + 2];
+        }
+      }
+      As[jq][il] = v.x;
+      As[jq + 1][il] = v.y;
+      As[jq + 2][il] = v.z;
+      As[jq + 3][il] = v.w;
+    }
+    for (int e = tid; e < CB * kTK; e += 256) {
+      const int c = e >> 4, jj = e & 15;
+      Ps[jj][c] = (c0 + c < k && j0 + jj < n) ? Pb[(size_t)(c0 + c) * n + j0 + jj] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < kTK; ++jj) {
+      float pv[CT], av[8];
+#pragma unroll
+      for (int v = 0; v < CT; ++v) pv[v] = Ps[jj][ty * CT + v];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) av[u] = As[jj][tx + 16 * u];
+#pragma unroll
+      for (int v = 0; v < CT; ++v)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[v][u] = fmaf(pv[v], av[u], acc[v][u]);
+    }
+    __syncthreads();
+  }
+  float* Ob = Out + (size_t)b * k * m;
+#pragma unroll
+  for (int v = 0; v < CT; ++v) {
+    const int c = c0 + ty * CT + v;
+    if (c >= k) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + tx + 16 * u;
+      if (i < m) Ob[(size_t)c * m + i] = acc[v][u];
+    }
+  }
+}
+
+// partial[b][tile] = sum over a [64 x 128] tile of (A - L R^T)^2 ; L [m][r], R [n][r]
+__global__ void __launch_bounds__(256) scw_residual_tiled_kernel(const float* __restrict__ A,
+                                                                 const float* __restrict__ L,
+                                                                 const float* __restrict__ R, int m, int n, int r,
+                                                                 double* __restrict__ part) {
+  __shared__ float Ls[kTK][64 + 4];
+  __shared__ float Rs[kTK][128 + 4];
+  __shared__ double red[256];
+  const int b = blockIdx.z;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 128;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const float* Lb = L + (size_t)b * m * r;
+  const float* Rb = R + (size_t)b * n * r;
+  float acc[4][8];
+#pragma unroll
+  for (int v = 0; v < 4; ++v)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
+  for (int cc0 = 0; cc0 < r; cc0 += kTK) {
+    for (int e = tid; e < 64 * kTK; e += 256) {
+      const int il = e >> 4, cc = e & 15;
+      Ls[cc][il] = (i0 + il < m && cc0 + cc < r) ? Lb[(size_t)(i0 + il) * r + cc0 + cc] : 0.f;
+    }
+    for (int e = tid; e < 128 * kTK; e += 256) {
+      const int jl = e >> 4, cc = e & 15;
+      Rs[cc][jl] = (j0 + jl < n && cc0 + cc < r) ? Rb[(size_t)(j0 + jl) * r + cc0 + cc] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < kTK; ++cc) {
+      float lv[4], rv[8];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) lv[v] = Ls[cc][ty * 4 + v];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) rv[u] = Rs[cc][tx + 16 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[v][u] = fmaf(lv[v], rv[u], acc[v][u]);
+    }
+    __syncthreads();
+  }
+  const float* Ab = A + (size_t)b * m * n;
+  double s = 0.0;
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    const int i = i0 + ty * 4 + v;
+    if (i >= m) continue;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + tx + 16 * u;
+      if (j < n) {
+        const double d = (double)Ab[(size_t)i * n + j] - (double)acc[v][u];
+        s += d * d;
+      }
+    }
+  }
+  red[tid] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) part[(size_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = red[0];
 }
 
 static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -282,8 +378,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   float* Vt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
   float* Zt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
   double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW_3, chunk * (4 * kk + 2 * k) * 8));
-  const int rows_per_block = 64;
-  const int tiles = (m + rows_per_block - 1) / rows_per_block;
+  const int tiles = (int)(nb(n, 128) * nb(m, 64));
   float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * r * 4));
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
   if (!Bm || !Vt || !Zt || !small || !Lw || !part) return TSK_ENOMEM;
@@ -295,8 +390,10 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   double* sig2 = mu + chunk * k;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(scw_vt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_vt_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_vt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr = true;
   }
   tsk_status st;
@@ -304,20 +401,19 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     const int bc = (int)std::min(chunk, B - b0);
     const float* Ac = A + (size_t)b0 * m * n;
     // 1. B = S A
-    dim3 gsa(nb(n, 128), bc);
-    if (k <= 32) scw_sa_kernel<32><<<gsa, 128, 0, s>>>(Ac, S, m, n, k, Bm);
-    else if (k <= 64) scw_sa_kernel<64><<<gsa, 128, 0, s>>>(Ac, S, m, n, k, Bm);
-    else scw_sa_kernel<128><<<gsa, 128, 0, s>>>(Ac, S, m, n, k, Bm);
+    if (k <= 32) scw_sa_tiled_kernel<32><<<dim3(nb(n, 128), 1, bc), 256, 0, s>>>(Ac, S, m, n, k, Bm);
+    else if (k <= 64) scw_sa_tiled_kernel<64><<<dim3(nb(n, 128), 1, bc), 256, 0, s>>>(Ac, S, m, n, k, Bm);
+    else scw_sa_tiled_kernel<64><<<dim3(nb(n, 128), nb(k, 64), bc), 256, 0, s>>>(Ac, S, m, n, k, Bm);
     // 2. orthonormal row basis of B
     launch_gram_rows(Bm, k, n, bc, Cb, s);
     ctx->count_launch(2);
     if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu)) != TSK_OK) return st;
-    scw_vt_kernel<<<dim3(nb(n, 256), bc), 256, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
+    if (k <= 64) scw_vt_kernel<64><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
+    else scw_vt_kernel<128><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
     // 3. Z^T = V^T A^T
-    dim3 gav(nb(m, 64), bc);
-    if (k <= 32) scw_av_kernel<32><<<gav, 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
-    else if (k <= 64) scw_av_kernel<64><<<gav, 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
-    else scw_av_kernel<128><<<gav, 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
+    if (k <= 32) scw_av_tiled_kernel<32><<<dim3(nb(m, 128), 1, bc), 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
+    else if (k <= 64) scw_av_tiled_kernel<64><<<dim3(nb(m, 128), 1, bc), 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
+    else scw_av_tiled_kernel<64><<<dim3(nb(m, 128), nb(k, 64), bc), 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
     // 4. SVD of AV through its Gram
     launch_gram_rows(Zt, k, m, bc, H, s);
     ctx->count_launch(3);
@@ -325,8 +421,13 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
-    scw_combine_kernel<<<dim3(nb(m, 256), bc), 256, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, Lc);
-    scw_combine_kernel<<<dim3(nb(n, 256), bc), 256, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, Rc);
+    if (k <= 64) {
+      scw_combine_kernel<64><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, Lc);
+      scw_combine_kernel<64><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, Rc);
+    } else {
+      scw_combine_kernel<128><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, Lc);
+      scw_combine_kernel<128><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, Rc);
+    }
     ctx->count_launch(2);
     if (sigma) {
       scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
@@ -334,10 +435,9 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     }
     // 6. dense residual
     if (err) {
-      dim3 gres(tiles, bc);
-      if (r <= 32) scw_residual_kernel<32><<<gres, 256, 0, s>>>(Ac, Lc, Rc, m, n, r, rows_per_block, part);
-      else scw_residual_kernel<64><<<gres, 256, 0, s>>>(Ac, Lc, Rc, m, n, r, rows_per_block, part);
-      scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, tiles, bc, err + b0);
+      dim3 gres(nb(n, 128), nb(m, 64), bc);
+      scw_residual_tiled_kernel<<<gres, 256, 0, s>>>(Ac, Lc, Rc, m, n, r, part);
+      scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
       ctx->count_launch(2);
     }
     if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
