@@ -241,6 +241,101 @@ __global__ void trsm_rlt_kernel(const double* __restrict__ Y, const double* __re
   for (int c = 0; c < p; ++c) out[c] = q[c];
 }
 
+// ---------------------------------------------------------------- Cholesky + inverse: Rinv = L^{-T}
+// One CTA (256 threads, 16 x 16 grid) per matrix; C and the factor live in shared memory.
+// Factorisation: right-looking with the column scaling deferred (step j updates the trailing
+// triangle with L_ij L_lj / d_j from the unscaled column j).  Inverse: forward elimination of
+// [L | I] row by row.  The column (row) consumed by each step is first copied into a separate
+// static shared array, so the compiler can prove the update's stores do not alias its operands.
+// Output Rinv[a][c] = Linv[c][a] (upper triangular): Q = Y Rinv has orthonormal columns when
+// C = Y^T Y.  flag as in chol_kernel.
+__global__ void __launch_bounds__(256) chol_inv2_kernel(const double* __restrict__ C, int p, double rel_tol,
+                                                        double* __restrict__ Rinv, int* __restrict__ flag) {
+  extern __shared__ double sm2[];
+  const int ld = p | 1;
+  double* Lm = sm2;                      // [p][ld]
+  double* X = sm2 + (size_t)p * ld;      // [p][ld]  L^{-1}
+  __shared__ double dmax;
+  __shared__ int fail;
+  __shared__ double colj[128];
+  const int b = blockIdx.x, tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const double* Cb = C + (size_t)b * p * p;
+  for (int e = tid; e < p * p; e += 256) {
+    const int i = e / p, l = e - (e / p) * p;
+    Lm[i * ld + l] = Cb[e];
+    X[i * ld + l] = (i == l) ? 1.0 : 0.0;
+  }
+  if (tid == 0) {
+    double d = 0;
+    for (int i = 0; i < p; ++i) d = fmax(d, Cb[(size_t)i * p + i]);
+    dmax = d;
+    fail = 0;
+  }
+  __syncthreads();
+  const double floor_piv = rel_tol * dmax;
+  for (int j = 0; j < p; ++j) {
+    double d = Lm[j * ld + j];
+    if (!(d > floor_piv)) {
+      if (tid == 0 && fail == 0) fail = j + 1;
+      d = fmax(dmax, 1e-300);
+      if (tid == 0) Lm[j * ld + j] = d;
+    }
+    const double inv_d = 1.0 / d;
+    for (int i = j + 1 + tid; i < p; i += 256) colj[i] = Lm[i * ld + j];
+    __syncthreads();
+    for (int i = j + 1 + ty; i < p; i += 16) {
+      const double f = colj[i] * inv_d;
+      double* row = Lm + i * ld;
+      for (int l = j + 1 + tx; l <= i; l += 16) row[l] -= f * colj[l];
+    }
+    __syncthreads();
+  }
+  // deferred scaling: L_ij = C'_ij / sqrt(d_j) for i > j, L_jj = sqrt(d_j)
+  for (int e = tid; e < p * p; e += 256) {
+    const int i = e / p, j = e - (e / p) * p;
+    if (j < i) Lm[i * ld + j] *= rsqrt(Lm[j * ld + j]);
+  }
+  __syncthreads();
+  for (int j = tid; j < p; j += 256) Lm[j * ld + j] = sqrt(Lm[j * ld + j]);
+  __syncthreads();
+  // forward elimination: row j of X scaled by 1/L_jj, then X[i,:] -= L_ij X[j,:] for i > j
+  for (int j = 0; j < p; ++j) {
+    const double ljj = Lm[j * ld + j];
+    for (int c = tid; c <= j; c += 256) {
+      const double v = X[j * ld + c] / ljj;
+      X[j * ld + c] = v;
+      colj[c] = v;
+    }
+    __syncthreads();
+    for (int i = j + 1 + ty; i < p; i += 16) {
+      const double lij = Lm[i * ld + j];
+      double* row = X + i * ld;
+      for (int c = tx; c <= j; c += 16) row[c] -= lij * colj[c];
+    }
+    __syncthreads();
+  }
+  double* Rb = Rinv + (size_t)b * p * p;
+  for (int e = tid; e < p * p; e += 256) {
+    const int a = e / p, c = e - (e / p) * p;
+    Rb[e] = X[c * ld + a];
+  }
+  if (tid == 0 && fail) flag[b] = fail;
+}
+
+tsk_status chol_inv2(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* Rinv, int* flag) {
+  const size_t smem = (size_t)2 * p * (p | 1) * sizeof(double);
+  if (smem > 220 * 1024 || p > 128) return TSK_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(chol_inv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) != cudaSuccess)
+      return TSK_ECUDA;
+    attr = true;
+  }
+  chol_inv2_kernel<<<batch, 256, smem, ctx->stream>>>(C, p, rel_tol, Rinv, flag);
+  ctx->count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
+}
+
 tsk_status chol(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* L, int* flag, int ws_id) {
   const size_t need = (size_t)p * p * sizeof(double);
   const int use_smem = need <= 200 * 1024;

@@ -16,4 +16,6 @@ tsk_status gemm_nn_f64(Ctx* ctx, const double* Z, long long ldz, long long sz, c
 tsk_status chol(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* L, int* flag, int ws_id);
 // Q = Y L^{-T} (Y, Q: m x p row-major; L: p x p lower), i.e. Q R = Y with R = L^T; p <= ~150
 tsk_status trsm_rlt(Ctx* ctx, const double* Y, const double* L, int m, int p, double* Q);
+// Cholesky C = L L^T and Rinv = L^{-T} (upper) in one CTA (p <= 116); flag as chol
+tsk_status chol_inv2(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* Rinv, int* flag);
 }  // namespace tsk

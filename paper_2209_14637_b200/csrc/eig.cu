@@ -144,22 +144,77 @@ __global__ void colscale_kernel(const double* __restrict__ Z, const double* __re
 // pass is already orthonormal to ~cond(Y)^2 eps; the second pass removes that residue.
 // flags[0..1] (device) receive the first failed pivot + 1 of each pass (0 = success): a failure
 // means rank(Y) < p, repaired by the caller.
-static tsk_status cholqr1(Ctx* ctx, const double* Y, double* Q, int m, int p, double* C, double* L, int* flags) {
-  tsk_status st;
-  if ((st = gemm_tn_f64(ctx, Y, p, 0, Y, p, 0, m, p, p, 1, C, p, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
-  if ((st = chol(ctx, C, p, 1, 1e-13, L, flags, WS_JACOBI)) != TSK_OK) return st;
-  return trsm_rlt(ctx, Y, L, m, p, Q);
+
+// G64[i][j] -= sum_t theta_t x_t[i] x_t[j]  (deflation of locked Ritz pairs; X: [m][ldx] columns t0..t1)
+__global__ void deflate_kernel(double* __restrict__ G, int m, const double* __restrict__ X, int ldx, int t0, int t1,
+                               const double* __restrict__ theta) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)m * m) return;
+  const int i = (int)(idx / m), j = (int)(idx % m);
+  double s = 0.0;
+  for (int t = t0; t < t1; ++t) s += theta[t] * X[(size_t)i * ldx + t] * X[(size_t)j * ldx + t];
+  G[idx] -= s;
 }
 
-static tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int m, int p, double* C, double* L,
-                          int* flags) {
+// Chebyshev three-term step:  Ynew = alpha (Z - c Y) - beta Yprev   (m x p, row-major)
+__global__ void cheb_step_kernel(const double* __restrict__ Z, const double* __restrict__ Yc,
+                                 const double* __restrict__ Yp, long long n, double c, double alpha, double beta,
+                                 double* __restrict__ Yn) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  const double v = alpha * (Z[idx] - c * Yc[idx]);
+  Yn[idx] = beta != 0.0 ? v - beta * Yp[idx] : v;
+}
+
+// column norms of Y (m x p) -> inverse norms (0 for a zero column); one block per column
+__global__ void inv_colnorm_kernel(const double* __restrict__ Y, int m, int p, double* __restrict__ inv) {
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double v = Y[(size_t)i * p + c];
+    s += v * v;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) inv[c] = red[0] > 0.0 ? 1.0 / sqrt(red[0]) : 0.0;
+}
+
+// copy columns [c0, c0+nc) of src [m][lds] to columns [d0, d0+nc) of dst [m][ldd]
+__global__ void copy_cols_kernel(const double* __restrict__ src, int lds, int c0, double* __restrict__ dst, int ldd,
+                                 int d0, int m, int nc) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)m * nc) return;
+  const int i = (int)(idx / nc), c = (int)(idx % nc);
+  dst[(size_t)i * ldd + d0 + c] = src[(size_t)i * lds + c0 + c];
+}
+
+// one CholQR pass Q = Y R^{-1}: C = Y^T Y (fp64), R^{-1} from one-CTA Cholesky + inverse, Q = Y R^{-1}
+// (parallel fp64 GEMM); for large blocks (p > 116) the row-parallel TRSM path is used instead.
+static tsk_status cholqr_pass(Ctx* ctx, const double* Y, double* Q, int m, int p, double* C, double* R, int* flag) {
   tsk_status st;
   if ((st = gemm_tn_f64(ctx, Y, p, 0, Y, p, 0, m, p, p, 1, C, p, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
-  if ((st = chol(ctx, C, p, 1, 1e-13, L, flags, WS_JACOBI)) != TSK_OK) return st;
-  if ((st = trsm_rlt(ctx, Y, L, m, p, Q1)) != TSK_OK) return st;
-  if ((st = gemm_tn_f64(ctx, Q1, p, 0, Q1, p, 0, m, p, p, 1, C, p, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
-  if ((st = chol(ctx, C, p, 1, 1e-13, L, flags + 1, WS_JACOBI)) != TSK_OK) return st;
-  return trsm_rlt(ctx, Q1, L, m, p, Q);
+  if ((size_t)2 * p * (p | 1) * 8 <= 220 * 1024 && p <= 128) {
+    if ((st = chol_inv2(ctx, C, p, 1, 1e-13, R, flag)) != TSK_OK) return st;
+    return gemm_nn_f64(ctx, Y, p, 0, R, p, 0, m, p, p, 1, nullptr, Q, p, 0);
+  }
+  if ((st = chol(ctx, C, p, 1, 1e-13, R, flag, WS_JACOBI)) != TSK_OK) return st;
+  return trsm_rlt(ctx, Y, R, m, p, Q);
+}
+
+static tsk_status cholqr1(Ctx* ctx, const double* Y, double* Q, int m, int p, double* C, double* R, int* flags) {
+  return cholqr_pass(ctx, Y, Q, m, p, C, R, flags);
+}
+
+static tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int m, int p, double* C, double* R,
+                          int* flags) {
+  tsk_status st;
+  if ((st = cholqr_pass(ctx, Y, Q1, m, p, C, R, flags)) != TSK_OK) return st;
+  return cholqr_pass(ctx, Q1, Q, m, p, C, R, flags + 1);
 }
 
 tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
@@ -203,117 +258,195 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
   const int ms = (m + 3) & ~3;
   const size_t mp = (size_t)m * p;
   // workspace carve-up
-  double* big = reinterpret_cast<double*>(ctx->workspace(WS_EIG_A, mp * 8 * 5));
-  double* small = reinterpret_cast<double*>(ctx->workspace(WS_EIG_B, ((size_t)p * p * 4 + p * 8) * 8 + 256));
+  double* big = reinterpret_cast<double*>(ctx->workspace(WS_EIG_A, mp * 8 * 8));
+  double* small = reinterpret_cast<double*>(ctx->workspace(WS_EIG_B, ((size_t)p * p * 4 + p * 12) * 8 + 256));
   float* G32 = reinterpret_cast<float*>(ctx->workspace(WS_EIG_G32, (size_t)m * ms * 4));
   float* Qt = reinterpret_cast<float*>(ctx->workspace(WS_EIG_Q32, (size_t)p * ms * 4));
+  double* Gd = reinterpret_cast<double*>(ctx->workspace(WS_EIG_C, (size_t)m * m * 8));
   double* hostbuf = reinterpret_cast<double*>(ctx->pinned((size_t)(4 * p + 16) * 8));
-  if (!big || !small || !G32 || !Qt || !hostbuf) return TSK_ENOMEM;
+  if (!big || !small || !G32 || !Qt || !Gd || !hostbuf) return TSK_ENOMEM;
   double *Q = big, *Z = big + mp, *X = big + 2 * mp, *Y = big + 3 * mp, *Q1 = big + 4 * mp;
+  double *Y0 = big + 5 * mp, *Y1 = big + 6 * mp, *Xl = big + 7 * mp;  // Xl: locked Ritz vectors [m][p]
   double *H = small, *W = small + (size_t)p * p, *C = small + 2 * (size_t)p * p, *Rinv = small + 3 * (size_t)p * p;
-  double *theta = small + 4 * (size_t)p * p, *invt = theta + p, *res = theta + 2 * p;
-  int* flags = reinterpret_cast<int*>(theta + 5 * p);
+  double *theta = small + 4 * (size_t)p * p, *invt = theta + p, *res = theta + 2 * p, *thl = theta + 3 * p;
+  double* ncol = theta + 4 * p;
+  int* flags = reinterpret_cast<int*>(theta + 6 * p);
 
-  g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(G64, m, ms, G32);
+  // The iteration works on the deflated Gram G' = G - sum_locked theta_t x_t x_t^T (fp64 master
+  // copy Gd, fp32 copy G32 for the tensor-core products).
+  cudaMemcpyAsync(Gd, G64, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, s);
+  g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(Gd, m, ms, G32);
   hash_fill_kernel<<<nblk((long long)mp, 256), 256, 0, s>>>(Y, m, p, 0x5EEDull, 1.0, 0);
   ctx->count_launch(2);
+  cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
   if ((st = cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags)) != TSK_OK) return st;
 
   GemmProblem gp;
   gp.X = G32;
   gp.Y = Qt;
   gp.M = m;
-  gp.N = p;
   gp.n = m;
   gp.D = 1;
   gp.x_row_stride = ms;
   gp.x_slice_stride = (long long)m * ms;
   gp.y_row_stride = ms;
-  gp.y_slice_stride = (long long)p * ms;
-  gp.sym = 0;
-  gp.out64 = Z;
-  gp.ldo64 = p;
   gp.min_chunks_per_unit = 2;
   gp.chain = 1;  // short TMEM chains: the eigensolver needs G Q to ~3e-7, not ~1e-6
 
-  // Rayleigh-Ritz (and the convergence test) every `rr_every` iterations; span(Q) -- and so
-  // the convergence of the subspace -- does not depend on the basis, so the iterations in
-  // between only orthonormalise Y = G Q diag(1/theta) (columns stay aligned with the last
-  // Ritz vectors, which keeps Y well conditioned).
-  const int rr_every = 4;
-  int it = 0;
+  // Z = G' B for an m x pa fp64 block B (fp32 copy for the tensor cores; B <- fp64(fp32(B)))
+  auto gq = [&](double* B, int pa) -> tsk_status {
+    q_to_f32t_kernel<<<nblk((long long)pa * ms, 256), 256, 0, s>>>(B, m, pa, ms, Qt);
+    ctx->count_launch();
+    gp.N = pa;
+    gp.y_slice_stride = (long long)pa * ms;
+    gp.out64 = Z;
+    gp.ldo64 = pa;
+    return gemm_tf32x3(ctx, gp);
+  };
+
+  // Outer iteration: Rayleigh-Ritz on span(Q) -> convergence test -> lock + deflate the leading
+  // converged Ritz pairs that sit well above the wanted edge -> Chebyshev filter of degree d on
+  // [0, b] (b = smallest Ritz value of the block) applied to the remaining Ritz vectors, with d
+  // the largest degree keeping the filter's dynamic range T_d(x_max) <= 1e6 (so CholQR2 stays
+  // accurate) -> CholQR2.  Deflating the dominant pairs (C3/C4: the frame mean is 1e4 x the rest)
+  // is what makes the filter usable; on its own each filter degree replaces d power steps.
+  int nl = 0;           // locked pairs
+  int pa = p;           // active block size
+  int outer = 0, products = 0;
   bool converged = false;
-  double max_res = 0.0, kyfan = 0.0;
+  double max_res = 0.0, kyfan = 0.0, theta_top = 0.0;
   int repairs = 0;
-  cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
-  for (it = 1; it <= max_iters; ++it) {
-    q_to_f32t_kernel<<<nblk((long long)p * ms, 256), 256, 0, s>>>(Q, m, p, ms, Qt);
+  for (outer = 1; outer <= max_iters; ++outer) {
+    const int kr = k - nl;  // wanted pairs still active
+    if ((st = gq(Q, pa)) != TSK_OK) return st;
+    ++products;
+    if ((st = gemm_tn_f64(ctx, Q, pa, 0, Z, pa, 0, m, pa, pa, 1, H, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
+    if ((st = jacobi_eig_batched(ctx, H, pa, 1, W, theta, nullptr, 1e-9)) != TSK_OK) return st;
+    inv_theta_kernel<<<nblk(pa, 128), 128, 0, s>>>(theta, pa, invt);
     ctx->count_launch();
-    if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;  // Z = G Q
-    const bool do_rr = (it % rr_every) == 1 || rr_every == 1 || it == max_iters;
-    if (!do_rr) {
-      colscale_kernel<<<nblk((long long)mp, 256), 256, 0, s>>>(Z, invt, m, p, Y);
-      ctx->count_launch();
-      // one CholQR pass between checks (Y is column-scaled, so orthonormal to ~cond(Y)^2 eps),
-      // two passes before the Rayleigh-Ritz check
-      const bool next_rr = ((it + 1) % rr_every) == 1 || it + 1 == max_iters;
-      if ((st = next_rr ? cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags) : cholqr1(ctx, Y, Q, m, p, C, Rinv, flags)) !=
-          TSK_OK)
-        return st;
-      continue;
-    }
-    if ((st = gemm_tn_f64(ctx, Q, p, 0, Z, p, 0, m, p, p, 1, H, p, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;  // H
-    // loose rotation threshold: the Rayleigh-Ritz basis only needs ~1e-9 accuracy (span(Q) carries the
-    // convergence; S is returned in fp32), and it saves most of the Jacobi sweeps
-    if ((st = jacobi_eig_batched(ctx, H, p, 1, W, theta, nullptr, 1e-9)) != TSK_OK) return st;
-    inv_theta_kernel<<<nblk(p, 128), 128, 0, s>>>(theta, p, invt);
+    if ((st = gemm_nn_f64(ctx, Z, pa, 0, W, pa, 0, m, pa, pa, 1, invt, Y, pa, 0)) != TSK_OK) return st;  // G'X/theta
+    if ((st = gemm_nn_f64(ctx, Q, pa, 0, W, pa, 0, m, pa, pa, 1, nullptr, X, pa, 0)) != TSK_OK) return st;  // X = QW
+    ritz_residual_kernel<<<kr, 256, 0, s>>>(Y, X, theta, m, pa, res);
     ctx->count_launch();
-    if ((st = gemm_nn_f64(ctx, Z, p, 0, W, p, 0, m, p, p, 1, invt, Y, p, 0)) != TSK_OK) return st;     // Y = GX/theta
-    if ((st = gemm_nn_f64(ctx, Q, p, 0, W, p, 0, m, p, p, 1, nullptr, X, p, 0)) != TSK_OK) return st;  // X = QW
-    ritz_residual_kernel<<<k, 256, 0, s>>>(Y, X, theta, m, p, res);
-    ctx->count_launch();
-    // host check: theta[0..k), res[0..k), pivot flags of the orthonormalisations since the last check
-    cudaMemcpyAsync(hostbuf, theta, (size_t)k * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hostbuf + p, res, (size_t)k * 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hostbuf, theta, (size_t)pa * 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hostbuf + p, res, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(hostbuf + 2 * p, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return TSK_ECUDA;
+    const double* hth = hostbuf;
+    const double* hres = hostbuf + p;
     const int* hflags = reinterpret_cast<const int*>(hostbuf + 2 * p);
-    const int ndeg = hflags[0] + hflags[1];
-    kyfan = 0.0;
+    if (nl == 0) theta_top = hth[0];
     max_res = 0.0;
-    for (int c = 0; c < k; ++c) {
-      kyfan += hostbuf[c];
-      max_res = std::max(max_res, hostbuf[p + c]);
-    }
-    max_res = hostbuf[0] > 0 ? max_res / hostbuf[0] : max_res;
-    if (getenv("TSK_EIG_TRACE")) {
-      int am = 0;
-      for (int c = 0; c < k; ++c)
-        if (hostbuf[p + c] > hostbuf[p + am]) am = c;
-      fprintf(stderr, "[eig] it=%d max_res=%.3e at c=%d theta_c=%.6e theta_0=%.6e theta_k-1=%.6e flags=%d\n", it,
-              max_res, am, hostbuf[am], hostbuf[0], hostbuf[k - 1], ndeg);
-    }
-    if (ndeg > 0) {
+    for (int c = 0; c < kr; ++c) max_res = std::max(max_res, hres[c]);
+    max_res /= theta_top > 0 ? theta_top : 1.0;
+    if (getenv("TSK_EIG_TRACE"))
+      fprintf(stderr, "[eig] outer=%d products=%d locked=%d max_res=%.3e theta0=%.4e theta_k=%.4e theta_p=%.4e\n",
+              outer, products, nl, max_res, hth[0], hth[kr - 1], hth[pa - 1]);
+    if (hflags[0] + hflags[1] > 0) {
       // rank-deficient block (rank(G) < p): perturb with fresh directions and re-orthonormalise
       if (++repairs > 8) return TSK_ECUDA;
-      hash_fill_kernel<<<nblk((long long)mp, 256), 256, 0, s>>>(Y, m, p, 0xBADC0DEull + repairs, 1e-3, 1);
+      cudaMemcpyAsync(Y, Q, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
+      hash_fill_kernel<<<nblk((long long)m * pa, 256), 256, 0, s>>>(Y, m, pa, 0xBADC0DEull + repairs, 1e-3, 1);
       ctx->count_launch();
-      if ((st = cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags)) != TSK_OK) return st;
+      if ((st = cholqr2(ctx, Y, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
       continue;
     }
     if (max_res <= tol) {
       converged = true;
       break;
     }
-    if (it == max_iters) break;
-    if ((st = cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags)) != TSK_OK) return st;
+    if (outer == max_iters) break;
+    // ---- lock the leading converged pairs well above the wanted edge (theta >= 2 theta_{k-1})
+    int nnew = 0;
+    while (nnew < kr - 1 && hres[nnew] <= tol * theta_top && hth[nnew] >= 2.0 * hth[kr - 1]) ++nnew;
+    const double* tha = theta;  // device Ritz values of the active block
+    int off = 0;                // first active column of X / theta after locking
+    if (nnew > 0) {
+      copy_cols_kernel<<<nblk((long long)m * nnew, 256), 256, 0, s>>>(X, pa, 0, Xl, p, nl, m, nnew);
+      cudaMemcpyAsync(thl + nl, theta, (size_t)nnew * 8, cudaMemcpyDeviceToDevice, s);
+      deflate_kernel<<<nblk((long long)m * m, 256), 256, 0, s>>>(Gd, m, X, pa, 0, nnew, theta);
+      g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(Gd, m, ms, G32);
+      ctx->count_launch(3);
+      nl += nnew;
+      off = nnew;
+    }
+    const int pn = pa - off;
+    // ---- Chebyshev filter on [0, b] applied to the remaining Ritz vectors X[:, off:pa]
+    const double b = hth[pa - 1];
+    const double xmax = 2.0 * hth[off] / b - 1.0;
+    int d = 1;
+    if (b > 0.0 && xmax > 1.0 + 1e-12) {
+      const double ach = acosh(xmax);
+      d = (int)std::floor(std::log(2e6) / ach);  // T_d(x) ~ exp(d acosh x) / 2 <= 1e6
+      d = std::max(1, std::min(d, 12));
+    }
+    copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(X, pa, off, Y0, pn, 0, m, pn);
+    ctx->count_launch();
+    if (d == 1) {
+      // plain step Y = G' X / theta (the scaled power step of the previous version)
+      copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(Y, pa, off, Y1, pn, 0, m, pn);
+      ctx->count_launch();
+    } else {
+      const double cc = 0.5 * b, ee = 0.5 * b;
+      double* Yprev = nullptr;
+      double* Ycur = Y0;
+      double* Ynext = Y1;
+      double* spare = Q1;  // free until the CholQR below
+      for (int j = 1; j <= d; ++j) {
+        if ((st = gq(Ycur, pn)) != TSK_OK) return st;
+        ++products;
+        const double alpha = (j == 1) ? 1.0 / ee : 2.0 / ee;
+        cheb_step_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(Z, Ycur, Yprev, (long long)m * pn, cc, alpha,
+                                                                       j == 1 ? 0.0 : 1.0, Ynext);
+        ctx->count_launch();
+        double* t = Yprev ? Yprev : spare;
+        Yprev = Ycur;
+        Ycur = Ynext;
+        Ynext = t;
+      }
+      // normalise the filtered columns (their norms spread up to T_d(x_max)) into Y1
+      inv_colnorm_kernel<<<pn, 256, 0, s>>>(Ycur, m, pn, ncol);
+      colscale_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(Ycur, ncol, m, pn, Y1);
+      ctx->count_launch(2);
+    }
+    pa = pn;
+    if (nl > 0) {
+      // keep the active block orthogonal to the locked vectors: Y1 -= Xl (Xl^T Y1)
+      if ((st = gemm_tn_f64(ctx, Xl, p, 0, Y1, pa, 0, m, nl, pa, 1, C, pa, 0, 0, WS_EIG_SMALL)) != TSK_OK) return st;
+      if ((st = gemm_nn_f64(ctx, Xl, p, 0, C, pa, 0, m, nl, pa, 1, nullptr, Q1, pa, 0)) != TSK_OK) return st;
+      cheb_step_kernel<<<nblk((long long)m * pa, 256), 256, 0, s>>>(Y1, Y1, Q1, (long long)m * pa, 0.0, 1.0, 1.0, Y1);
+      ctx->count_launch();
+    }
+    if ((st = cholqr2(ctx, Y1, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
+    (void)tha;
   }
-  write_sketch_kernel<<<k, 256, 0, s>>>(X, m, p, S);
+  // output: locked pairs first (largest), then the leading active Ritz pairs; a final CholQR2 of
+  // the combined k columns (Gram-Schmidt order: locked columns are kept, active ones are made
+  // orthogonal to them) removes the residual locked/active coupling of the deflated iteration
+  const int kr = k - nl;
+  double* Xo = Y0;
+  if (nl > 0) copy_cols_kernel<<<nblk((long long)m * nl, 256), 256, 0, s>>>(Xl, p, 0, Xo, k, 0, m, nl);
+  copy_cols_kernel<<<nblk((long long)m * kr, 256), 256, 0, s>>>(X, pa, 0, Xo, k, nl, m, kr);
+  ctx->count_launch(2);
+  if (nl > 0) {
+    if ((st = cholqr2(ctx, Xo, Q1, Y1, m, k, C, Rinv, flags)) != TSK_OK) return st;
+    Xo = Y1;
+  }
+  write_sketch_kernel<<<k, 256, 0, s>>>(Xo, m, k, S);
   ctx->count_launch();
-  if (lambda) cudaMemcpyAsync(lambda, theta, (size_t)k * 8, cudaMemcpyDeviceToDevice, s);
+  if (lambda) {
+    if (nl > 0) cudaMemcpyAsync(lambda, thl, (size_t)nl * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(lambda + nl, theta, (size_t)kr * 8, cudaMemcpyDeviceToDevice, s);
+  }
   if (info) {
-    info->iters = std::min(it, max_iters);
+    info->iters = products;
+    std::vector<double> hl(k);
+    cudaMemcpyAsync(hl.data(), thl, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hl.data() + nl, theta, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    kyfan = 0.0;
+    for (double v : hl) kyfan += v;
     info->kyfan = kyfan;
     info->max_resid = max_res;
   }
