@@ -55,9 +55,17 @@ struct GemmArgs {
   int lag;       // drift throttle: max chunks a unit may run ahead of its K-split peers (0 = off)
   double* part;  // [U][128][128] fp64 partials
   unsigned* progress;  // [U] chunks issued per unit (drift throttle)
+  int batch;     // 0: the D slices are contracted; 1: D independent problems (slice z = problem b)
+  int T0;        // tiles per problem (batched)
+  int bn;        // MMA N: 128, or 64 for narrow outputs (TS kernel)
+  int Mv, Nv;    // valid output extents (direct output)
+  float* dout;   // direct fp32 output, transposed: dout[b * dstride + col * ldd + row] (requires S == 1)
+  long long dstride;
+  int ldd;
 };
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& bi, int& bj) {
+  if (a.batch) t %= a.T0;
   if (a.sym) {
     int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
     while ((i + 1) * (i + 2) / 2 <= t) ++i;
@@ -73,8 +81,10 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& bi, i
 __device__ __forceinline__ void unit_range(const GemmArgs& a, int u, int& t, long long& q0, long long& q1) {
   t = u % a.T;
   int s = u / a.T;
-  q0 = (long long)s * a.Kc / a.S;
-  q1 = (long long)(s + 1) * a.Kc / a.S;
+  // batched: tile t belongs to problem b = t / T0, whose K range is the chunks of slice b only
+  const long long base = a.batch ? (long long)(t / a.T0) * a.cps : 0;
+  q0 = base + (long long)s * a.Kc / a.S;
+  q1 = base + (long long)(s + 1) * a.Kc / a.S;
 }
 
 // Warp roles (16 warps): 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle,
@@ -360,6 +370,7 @@ constexpr int kTsSmemBytes = (kRawStages * 2 + kTsLoStages) * kTileBytes + 1024 
 constexpr uint32_t kTsAccCols = 128;
 constexpr uint32_t kTsAStageCols = 64;
 
+template <bool kN64>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                           const GemmArgs a) {
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
           tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
-          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * kBN, z);
+          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * a.bn, z);
         }
         if (++st == kRawStages) { st = 0; ph ^= 1; }
         const unsigned done = (unsigned)(q - q0 + 1);
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (elect_one()) {
-      const uint32_t idesc = idesc_tf32(kBM, kBN);
+      const uint32_t idesc = idesc_tf32(kBM, (uint32_t)a.bn);
       int rs = 0, ls = 0;
       uint32_t rph = 0, lph = 0;
       int ab = 0;
@@ -469,7 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mbar_wait(&lfull[ls], lph);  // transform done: implies the raw stage landed
           tc_fence_after();
+          // bn = 128: one accumulator per buffer; bn = 64: separate H H^T and cross accumulators
+          // (the truncating accumulation error then comes from the H H^T chain only)
           const uint32_t d = tmem_base + (uint32_t)ab * kTsAccCols;
+          const uint32_t dx = kN64 ? d + 64 : d;
           const uint32_t a_hi = tmem_base + 2 * kTsAccCols + (uint32_t)ls * kTsAStageCols;
           const uint32_t a_lo = a_hi + 32;
           const uint64_t yh = sw128_kmajor_desc(smem_u32(raw_ptr(rs, diag ? 0 : 1)));
@@ -477,9 +491,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32 >> 4);  // +32 B per K=8 step inside the swizzle atom
-            mma_tf32_ts(d, a_hi + kk * 8, yh + adv, idesc, (cpos > 0 || kk > 0) ? 1u : 0u);
-            mma_tf32_ts(d, a_hi + kk * 8, yl + adv, idesc, 1u);
-            mma_tf32_ts(d, a_lo + kk * 8, yh + adv, idesc, 1u);
+            const uint32_t acc = (cpos > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32_ts(d, a_hi + kk * 8, yh + adv, idesc, acc);
+            mma_tf32_ts(dx, a_hi + kk * 8, yl + adv, idesc, kN64 ? acc : 1u);
+            mma_tf32_ts(dx, a_lo + kk * 8, yh + adv, idesc, 1u);
           }
           mma_commit(&rempty[rs]);
           if (++rs == kRawStages) { rs = 0; rph ^= 1; }
@@ -561,6 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quad * 32 + lane;
     int ab = 0;
     uint32_t aph = 0;
+    const bool has_cols = col0 < a.bn;
     for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
       int t;
       long long q0, q1;
@@ -576,18 +592,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&accf[ab], aph);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)ab * kTsAccCols + col0;
+        if (has_cols) {
+          if constexpr (kN64) {  // separate accumulators: columns [0,64) = H H^T, [64,128) = cross terms
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + h * 32, r);
-          tmem_ld_wait();
+            for (int h = 0; h < 2; ++h) {
+              uint32_t r[32], x[32];
+              tmem_ld_32x32b_x32(taddr + h * 32, r);
+              tmem_ld_32x32b_x32(taddr + 64 + h * 32, x);
+              tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]);
+              for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]) + __uint_as_float(x[i]);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(taddr + h * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]);
+            }
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acce[ab]);
         if (++ab == 2) { ab = 0; aph ^= 1; }
+        if (a.dout) continue;  // direct output: keep summing in fp32, store once at the end
         if (++cin == a.fold || c + 1 == nchains) {
           const uint64_t pol = l2_policy_evict_last();
 #pragma unroll
@@ -608,6 +639,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           first_fold = false;
           cin = 0;
+        }
+      }
+      if (a.dout && has_cols) {
+        // transposed store: for a fixed column, the 32 lanes (consecutive rows) write contiguously
+        int bi, bj;
+        tile_coords(a, t, bi, bj);
+        const int b = a.batch ? t / a.T0 : 0;
+        const int gr = bi * kBM + row;
+        float* ob = a.dout + (size_t)b * a.dstride;
+        if (gr < a.Mv) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const int gc = bj * a.bn + col0 + i;
+            if (col0 + i < a.bn && gc < a.Nv) ob[(size_t)gc * a.ldd + gr] = sum[i];
+          }
         }
       }
     }
@@ -703,22 +749,38 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) return TSK_ECUDA;
 
   GemmArgs a{};
+  a.bn = (p.bn == 64 && !p.sym) ? 64 : 128;
   const int mb = (p.M + kBM - 1) / kBM;
-  const int nb = (p.N + kBN - 1) / kBN;
+  const int nb = (p.N + a.bn - 1) / a.bn;
   a.sym = p.sym;
   a.nb = nb;
-  a.T = p.sym ? mb * (mb + 1) / 2 : mb * nb;
   a.cps = (p.n + kBK - 1) / kBK;
-  a.Kc = (long long)p.D * a.cps;
-  a.S = p.splits > 0 ? p.splits : choose_splits(a.T, a.Kc, ctx->num_sms, p.min_chunks_per_unit > 0 ? p.min_chunks_per_unit : 8);
-  if (a.S > a.Kc) a.S = (int)a.Kc;
+  if (p.batch) {
+    // D independent problems; one unit per (problem, tile), results stored directly (fp32)
+    if (p.sym || !p.dout) return TSK_EINVAL;
+    a.batch = 1;
+    a.T0 = mb * nb;
+    a.T = (int)(p.D * a.T0);
+    a.Kc = a.cps;
+    a.S = 1;
+  } else {
+    a.T = p.sym ? mb * (mb + 1) / 2 : mb * nb;
+    a.Kc = (long long)p.D * a.cps;
+    a.S = p.splits > 0 ? p.splits : choose_splits(a.T, a.Kc, ctx->num_sms, p.min_chunks_per_unit > 0 ? p.min_chunks_per_unit : 8);
+    if (a.S > a.Kc) a.S = (int)a.Kc;
+  }
+  a.Mv = p.M;
+  a.Nv = p.N;
+  a.dout = p.dout;
+  a.dstride = p.dstride;
+  a.ldd = p.ldd;
   a.U = a.S * a.T;
   a.chain = p.chain > 0 ? p.chain : 4;
   a.fold = p.fold > 0 ? p.fold : 16;
   a.products = p.products == 1 ? 1 : 3;
   a.raw = p.raw;
-  a.lag = p.lag >= 0 ? p.lag : 64;
-  const size_t part_bytes = (size_t)a.U * kBM * kBN * sizeof(double);
+  a.lag = a.batch ? 0 : (p.lag >= 0 ? p.lag : 64);
+  const size_t part_bytes = a.dout ? 256 : (size_t)a.U * kBM * kBN * sizeof(double);
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_GEMM_PARTIAL, part_bytes));
   if (!part) return TSK_ENOMEM;
   a.part = part;
@@ -731,19 +793,35 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
             cudaSuccess ||
-        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes) !=
-            cudaSuccess)
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTsSmemBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTsSmemBytes) != cudaSuccess)
       return TSK_ECUDA;
     attr_set = true;
   }
   const int grid = std::min(a.U, ctx->num_sms);
   // production: TS variant (A operand from TMEM); the SS variant serves the diagnostic modes
-  if (a.products == 3 && !a.raw && !p.ss)
-    gemm_tf32x3_ts_kernel<<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
-  else
+  if (a.products == 3 && !a.raw && !p.ss) {
+    if (a.bn == 64)
+      gemm_tf32x3_ts_kernel<true><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+    else
+      gemm_tf32x3_ts_kernel<false><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+  } else {
+    if (a.batch || a.bn != 128 || a.dout) return TSK_EINVAL;  // diagnostic SS kernel: plain problems only
     gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(mx, my, a);
+  }
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   ctx->count_launch();
+  if (a.dout) {
+    if (p.info) {
+      p.info->splits = a.S;
+      p.info->units = a.U;
+      p.info->grid = grid;
+      p.info->tiles = a.T;
+    }
+    return TSK_OK;
+  }
 
   dim3 fb(32, 8);
   dim3 fg((p.N + 31) / 32, (p.M + 7) / 8);

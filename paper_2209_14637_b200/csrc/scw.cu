@@ -407,17 +407,37 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     // 2. orthonormal row basis of B
     launch_gram_rows(Bm, k, n, bc, Cb, s);
     ctx->count_launch(2);
-    if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu)) != TSK_OK) return st;
+    // rotation threshold 1e-10: V V^T - I is bounded by it (exactly orthogonal rotations), far below
+    // what the 1e-4 SCW-error parity needs, and it saves ~40% of the sweeps of 1e-13
+    if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) return st;
     if (k <= 64) scw_vt_kernel<64><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
     else scw_vt_kernel<128><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
     // 3. Z^T = V^T A^T
-    if (k <= 32) scw_av_tiled_kernel<32><<<dim3(nb(m, 128), 1, bc), 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
-    else if (k <= 64) scw_av_tiled_kernel<64><<<dim3(nb(m, 128), 1, bc), 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
-    else scw_av_tiled_kernel<64><<<dim3(nb(m, 128), nb(k, 64), bc), 256, 0, s>>>(Ac, Vt, m, n, k, Zt);
+    {
+      // Z^T[b] = V^T[b] A[b]^T on tcgen05 (3xTF32): X = A_b (m rows, K = n), Y = V^T_b (k rows),
+      // one unit per (matrix, 128-row tile), result stored transposed as Z^T [k][m]
+      GemmProblem gp;
+      gp.X = Ac;
+      gp.Y = Vt;
+      gp.M = m;
+      gp.N = k;
+      gp.n = n;
+      gp.D = bc;
+      gp.x_row_stride = n;
+      gp.x_slice_stride = (long long)m * n;
+      gp.y_row_stride = n;
+      gp.y_slice_stride = (long long)k * n;
+      gp.batch = 1;
+      gp.bn = k <= 64 ? 64 : 128;
+      gp.dout = Zt;
+      gp.dstride = (long long)k * m;
+      gp.ldd = m;
+      if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
+    }
     // 4. SVD of AV through its Gram
     launch_gram_rows(Zt, k, m, bc, H, s);
     ctx->count_launch(3);
-    if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2)) != TSK_OK) return st;
+    if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10)) != TSK_OK) return st;
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;

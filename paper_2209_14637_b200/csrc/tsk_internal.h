@@ -103,6 +103,11 @@ struct GemmProblem {
   int raw = 0;
   int lag = -1;  // drift throttle (chunks); -1 = default, 0 = off
   int ss = 0;    // 1: force the SS kernel variant (A operand from shared memory)
+  int batch = 0;          // 1: D independent problems (no contraction over slices)
+  int bn = 128;           // MMA N tile: 128 or 64
+  float* dout = nullptr;  // direct fp32 output, transposed: dout[b * dstride + col * ldd + row]
+  long long dstride = 0;
+  int ldd = 0;
   GemmInfo* info = nullptr;
 };
 
