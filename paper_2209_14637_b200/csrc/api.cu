@@ -456,6 +456,8 @@ tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, 
   p.products = (mode & 2) ? 1 : 3;
   p.lag = (mode & 4) ? 0 : -1;
   p.ss = (mode & 8) ? 1 : 0;
+  p.one_cta = (mode & 16) ? 1 : 0;
+  p.spin_waits = (mode & 32) ? 1 : 0;
   return tsk::gemm_tf32x3(&ctx->c, p);
 }
 

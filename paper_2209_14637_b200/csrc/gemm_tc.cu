@@ -297,7 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) sum[i] = 0.f;
-      int cin = 0;
+      // staggered folds: epilogue warp e folds (fp32 -> fp64 reductions at L2) at chains offset by
+      // e * fold / 8, so no single accumulator drain carries all the L2 reductions of a fold
+      int cin = (e * a.fold) / 8;
       bool first_fold = true;
       double* prow = a.part + (size_t)u * (kBM * kBN) + (size_t)row * kBN + col0;
       for (long long c = 0; c < nchains; ++c) {
@@ -329,17 +331,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t pol = l2_policy_evict_last();
 #pragma unroll
           for (int i = 0; i < 64; i += 2) {
-            double2* p2 = reinterpret_cast<double2*>(prow + i);
-            double2 v;
             if (first_fold) {
-              v.x = (double)sum[i];
-              v.y = (double)sum[i + 1];
+              st_f64x2_hint(reinterpret_cast<double2*>(prow + i), make_double2((double)sum[i], (double)sum[i + 1]), pol);
             } else {
-              v = ld_f64x2_hint(p2, pol);
-              v.x += (double)sum[i];
-              v.y += (double)sum[i + 1];
+              red_add_f64_hint(prow + i, (double)sum[i], pol);
+              red_add_f64_hint(prow + i + 1, (double)sum[i + 1], pol);
             }
-            st_f64x2_hint(p2, v, pol);
             sum[i] = 0.f;
             sum[i + 1] = 0.f;
           }
@@ -585,7 +582,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sum[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) sum[i] = 0.f;
-      int cin = 0;
+      // staggered folds: epilogue warp e folds (fp32 -> fp64 reductions at L2) at chains offset by
+      // e * fold / 8, so no single accumulator drain carries all the L2 reductions of a fold
+      int cin = (e * a.fold) / 8;
       bool first_fold = true;
       double* prow = a.part + (size_t)u * (kBM * kBN) + (size_t)row * kBN + col0;
       for (long long c = 0; c < nchains; ++c) {
@@ -623,17 +622,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t pol = l2_policy_evict_last();
 #pragma unroll
           for (int i = 0; i < 64; i += 2) {
-            double2* p2 = reinterpret_cast<double2*>(prow + i);
-            double2 v;
             if (first_fold) {
-              v.x = (double)sum[i];
-              v.y = (double)sum[i + 1];
+              st_f64x2_hint(reinterpret_cast<double2*>(prow + i), make_double2((double)sum[i], (double)sum[i + 1]), pol);
             } else {
-              v = ld_f64x2_hint(p2, pol);
-              v.x += (double)sum[i];
-              v.y += (double)sum[i + 1];
+              red_add_f64_hint(prow + i, (double)sum[i], pol);
+              red_add_f64_hint(prow + i + 1, (double)sum[i + 1], pol);
             }
-            st_f64x2_hint(p2, v, pol);
             sum[i] = 0.f;
             sum[i + 1] = 0.f;
           }
@@ -744,6 +738,8 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
       (p.y_slice_stride % 4) || (reinterpret_cast<uintptr_t>(p.X) & 15) || (reinterpret_cast<uintptr_t>(p.Y) & 15))
     return TSK_ESHAPE;
   if (p.sym && (p.X != p.Y || p.M != p.N)) return TSK_EINVAL;
+  // production symmetric Gram: CTA pairs (gram_pair.cu)
+  if (p.sym && p.products == 3 && !p.raw && !p.ss && !p.one_cta && !p.batch) return gram_pair(ctx, p);
   CUtensorMap mx, my;
   if (!make_map_3d(&mx, p.X, p.n, p.M, p.D, p.x_row_stride, p.x_slice_stride)) return TSK_ECUDA;
   if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) return TSK_ECUDA;
@@ -776,7 +772,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.ldd = p.ldd;
   a.U = a.S * a.T;
   a.chain = p.chain > 0 ? p.chain : 4;
-  a.fold = p.fold > 0 ? p.fold : 16;
+  a.fold = p.fold > 0 ? p.fold : 64;
   a.products = p.products == 1 ? 1 : 3;
   a.raw = p.raw;
   a.lag = a.batch ? 0 : (p.lag >= 0 ? p.lag : 64);

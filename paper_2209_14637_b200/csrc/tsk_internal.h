@@ -30,6 +30,7 @@ enum WorkspaceId {
   WS_GRAM,       // fp64 Gram for sketch_train
   WS_JACOBI,
   WS_GEMM_PROGRESS,
+  WS_GRAM_SCHED,   // pair-Gram schedule (units, tile map)
   WS_COUNT
 };
 
@@ -75,6 +76,9 @@ struct Ctx {
     return host_pinned;
   }
   void count_launch(int n = 1) { launches += n; }
+  // pair-Gram schedule last uploaded to ws[WS_GRAM_SCHED] (pointer + host schedule version)
+  const void* gram_sched_dev = nullptr;
+  long long gram_sched_ver = -1;
 };
 
 struct GemmInfo {
@@ -103,6 +107,8 @@ struct GemmProblem {
   int raw = 0;
   int lag = -1;  // drift throttle (chunks); -1 = default, 0 = off
   int ss = 0;    // 1: force the SS kernel variant (A operand from shared memory)
+  int spin_waits = 0;  // pair Gram: mbarrier waits without a suspend-time hint (diagnostics)
+  int one_cta = 0;  // 1: symmetric Gram on the 1-CTA TS kernel instead of CTA pairs (diagnostics)
   int batch = 0;          // 1: D independent problems (no contraction over slices)
   int bn = 128;           // MMA N tile: 128 or 64
   float* dout = nullptr;  // direct fp32 output, transposed: dout[b * dstride + col * ldd + row]
@@ -112,6 +118,8 @@ struct GemmProblem {
 };
 
 tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p);
+// symmetric Gram on CTA pairs (tcgen05 cta_group::2), gram_pair.cu
+tsk_status gram_pair(Ctx* ctx, const GemmProblem& p);
 
 // eigensolver (eig.cu)
 tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda, const tsk_train_opts* o,
