@@ -60,6 +60,8 @@ struct GemmArgs {
   int bn;        // MMA N: 128, or 64 for narrow outputs (TS kernel)
   int Mv, Nv;    // valid output extents (direct output)
   float* dout;   // direct fp32 output, transposed: dout[b * dstride + col * ldd + row] (requires S == 1)
+  int xt;        // X operand stored transposed ([z][K][M], M contiguous): the transform reads tile columns
+  int ybc;       // Y broadcast: every slice z uses Y slice 0
   long long dstride;
   int ldd;
 };
@@ -329,17 +331,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++cin == a.fold || c + 1 == nchains) {
           // partial-sum lines are re-read every fold: keep them in L2 against the streaming operands
           const uint64_t pol = l2_policy_evict_last();
+          if (first_fold) {
 #pragma unroll
-          for (int i = 0; i < 64; i += 2) {
-            if (first_fold) {
+            for (int i = 0; i < 64; i += 2)
               st_f64x2_hint(reinterpret_cast<double2*>(prow + i), make_double2((double)sum[i], (double)sum[i + 1]), pol);
-            } else {
-              red_add_f64_hint(prow + i, (double)sum[i], pol);
-              red_add_f64_hint(prow + i + 1, (double)sum[i + 1], pol);
-            }
-            sum[i] = 0.f;
-            sum[i + 1] = 0.f;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) red_add_f64_hint(prow + i, (double)sum[i], pol);
           }
+#pragma unroll
+          for (int i = 0; i < 64; ++i) sum[i] = 0.f;
           first_fold = false;
           cin = 0;
         }
@@ -431,8 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&rfull[st], diag ? kTileBytes : 2 * kTileBytes);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
-          tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
-          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * a.bn, z);
+          if (a.xt) tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], bi * kBM, kc, z);  // box {128 M, 32 K}
+          else tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
+          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * a.bn, a.ybc ? 0 : z);
         }
         if (++st == kRawStages) { st = 0; ph ^= 1; }
         const unsigned done = (unsigned)(q - q0 + 1);
@@ -521,19 +523,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&rfull[rs], rph);
         mbar_wait(&lempty[ls], lph ^ 1);
         tc_fence_after();
-        // (1) row tt of X (128-B swizzled row: 16-B chunk c at position c ^ (tt & 7))
+        // (1) row tt of X (128-B swizzled row: 16-B chunk c at position c ^ (tt & 7)); for a
+        // transposed X the raw tile is [32 K][128 M] unswizzled and row tt of X is column tt
         {
-          const uint32_t xrow = smem_u32(raw_ptr(rs, 0)) + (uint32_t)tt * 128u;
           uint32_t hi[32], lo[32];
+          if (a.xt) {
+            const float* xcol = reinterpret_cast<const float*>(raw_ptr(rs, 0)) + tt;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 v = lds_f4(xrow + (uint32_t)((c ^ (tt & 7)) * 16));
-            const float e[4] = {v.x, v.y, v.z, v.w};
+            for (int c = 0; c < 32; ++c) {
+              const float e = xcol[c * kBM];
+              const uint32_t h = __float_as_uint(e) & 0xFFFFE000u;
+              hi[c] = h;
+              lo[c] = __float_as_uint(e - __uint_as_float(h));
+            }
+          } else {
+            const uint32_t xrow = smem_u32(raw_ptr(rs, 0)) + (uint32_t)tt * 128u;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t h = __float_as_uint(e[j]) & 0xFFFFE000u;
-              hi[c * 4 + j] = h;
-              lo[c * 4 + j] = __float_as_uint(e[j] - __uint_as_float(h));
+            for (int c = 0; c < 8; ++c) {
+              const float4 v = lds_f4(xrow + (uint32_t)((c ^ (tt & 7)) * 16));
+              const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t h = __float_as_uint(e[j]) & 0xFFFFE000u;
+                hi[c * 4 + j] = h;
+                lo[c * 4 + j] = __float_as_uint(e[j] - __uint_as_float(h));
+              }
             }
           }
           const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + 2 * kTsAccCols + (uint32_t)ls * kTsAStageCols;
@@ -595,12 +609,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (kN64) {  // separate accumulators: columns [0,64) = H H^T, [64,128) = cross terms
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              uint32_t r[32], x[32];
+              uint32_t r[32];
               tmem_ld_32x32b_x32(taddr + h * 32, r);
-              tmem_ld_32x32b_x32(taddr + 64 + h * 32, x);
+              tmem_ld_wait();
+              float t[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) t[i] = __uint_as_float(r[i]);
+              tmem_ld_32x32b_x32(taddr + 64 + h * 32, r);
               tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) sum[h * 32 + i] += __uint_as_float(r[i]) + __uint_as_float(x[i]);
+              for (int i = 0; i < 32; ++i) sum[h * 32 + i] += t[i] + __uint_as_float(r[i]);
             }
           } else {
 #pragma unroll
@@ -620,17 +638,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.dout) continue;  // direct output: keep summing in fp32, store once at the end
         if (++cin == a.fold || c + 1 == nchains) {
           const uint64_t pol = l2_policy_evict_last();
+          if (first_fold) {
 #pragma unroll
-          for (int i = 0; i < 64; i += 2) {
-            if (first_fold) {
+            for (int i = 0; i < 64; i += 2)
               st_f64x2_hint(reinterpret_cast<double2*>(prow + i), make_double2((double)sum[i], (double)sum[i + 1]), pol);
-            } else {
-              red_add_f64_hint(prow + i, (double)sum[i], pol);
-              red_add_f64_hint(prow + i + 1, (double)sum[i + 1], pol);
-            }
-            sum[i] = 0.f;
-            sum[i + 1] = 0.f;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) red_add_f64_hint(prow + i, (double)sum[i], pol);
           }
+#pragma unroll
+          for (int i = 0; i < 64; ++i) sum[i] = 0.f;
           first_fold = false;
           cin = 0;
         }
@@ -741,8 +758,30 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   // production symmetric Gram: CTA pairs (gram_pair.cu)
   if (p.sym && p.products == 3 && !p.raw && !p.ss && !p.one_cta && !p.batch) return gram_pair(ctx, p);
   CUtensorMap mx, my;
-  if (!make_map_3d(&mx, p.X, p.n, p.M, p.D, p.x_row_stride, p.x_slice_stride)) return TSK_ECUDA;
-  if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) return TSK_ECUDA;
+  if (p.xt) {
+    // transposed X: [D][K = n][M] with M contiguous (x_row_stride = stride between K rows);
+    // box {128 M, 32 K}, no swizzle (the transform reads tile columns, 4-byte lanes: no conflicts)
+    if (p.sym || p.ss || p.products != 3 || p.raw || (p.x_row_stride % 4) || (p.M % 4)) return TSK_EINVAL;
+    auto enc = get_encode_fn();
+    if (!enc) return TSK_ECUDA;
+    cuuint64_t dims[3] = {(cuuint64_t)p.M, (cuuint64_t)p.n, (cuuint64_t)p.D};
+    cuuint64_t strides[2] = {(cuuint64_t)(p.x_row_stride * 4), (cuuint64_t)(p.x_slice_stride * 4)};
+    cuuint32_t box[3] = {(cuuint32_t)kBM, (cuuint32_t)kBK, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p.X), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: transposed X tensor map rejected\n");
+      return TSK_ECUDA;
+    }
+  } else if (!make_map_3d(&mx, p.X, p.n, p.M, p.D, p.x_row_stride, p.x_slice_stride)) {
+    if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: X tensor map rejected\n");
+    return TSK_ECUDA;
+  }
+  if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) {
+    if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: Y tensor map rejected\n");
+    return TSK_ECUDA;
+  }
 
   GemmArgs a{};
   a.bn = (p.bn == 64 && !p.sym) ? 64 : 128;
@@ -767,6 +806,8 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   }
   a.Mv = p.M;
   a.Nv = p.N;
+  a.xt = p.xt;
+  a.ybc = p.ybc;
   a.dout = p.dout;
   a.dstride = p.dstride;
   a.ldd = p.ldd;
@@ -807,7 +848,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
     if (a.batch || a.bn != 128 || a.dout) return TSK_EINVAL;  // diagnostic SS kernel: plain problems only
     gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(mx, my, a);
   }
-  if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
+  if (launch_status("gemm_tf32x3") != TSK_OK) return TSK_ECUDA;
   ctx->count_launch();
   if (a.dout) {
     if (p.info) {

@@ -380,17 +380,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (++ab == 2) { ab = 0; aph ^= 1; }
         if (++cin == a.fold || c + 1 == nchains) {
           const uint64_t pol = l2_policy_evict_last();
+          if (first_fold) {
 #pragma unroll
-          for (int i = 0; i < 64; i += 2) {
-            if (first_fold) {
+            for (int i = 0; i < 64; i += 2)
               st_f64x2_hint(reinterpret_cast<double2*>(prow + i), make_double2((double)sum[i], (double)sum[i + 1]), pol);
-            } else {
-              red_add_f64_hint(prow + i, (double)sum[i], pol);
-              red_add_f64_hint(prow + i + 1, (double)sum[i + 1], pol);
-            }
-            sum[i] = 0.f;
-            sum[i + 1] = 0.f;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) red_add_f64_hint(prow + i, (double)sum[i], pol);
           }
+#pragma unroll
+          for (int i = 0; i < 64; ++i) sum[i] = 0.f;
           first_fold = false;
           cin = 0;
         }

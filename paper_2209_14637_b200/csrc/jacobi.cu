@@ -11,6 +11,7 @@
 // fit, else in a global (L2-resident) scratch.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ptx.cuh"
 #include "tsk_internal.h"
@@ -89,11 +90,12 @@ __global__ void __launch_bounds__(kJacThreads)
             double c = 1.0, s = 0.0;
             if (hl == 0) {
               const double aii = A[i * ld + i], ajj = A[j * ld + j], aij = A[i * ld + j];
-              if (fabs(aij) > fmax(tol * sqrt(fabs(aii * ajj)), floor_abs)) {
+              // |A_ij| > max(tol sqrt|A_ii A_jj|, floor), squared: no fp64 square root on the chain
+              if (aij * aij > fmax(tol * tol * fabs(aii * ajj), floor_abs * floor_abs)) {
                 // tan of the annihilating angle, in fp32 (the MUFU path; ~1e-7 relative).  Any t
                 // gives an exactly orthogonal fp64 rotation (c^2 + s^2 = 1 to fp64 rounding); the
                 // residual ~1e-7 A_ij it leaves is removed by the quadratically convergent sweeps.
-                const float tau = (float)((ajj - aii) / (2.0 * aij));
+                const float tau = __fdividef((float)(ajj - aii), (float)(2.0 * aij));
                 const float tf = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
                 const double t = (double)tf;
                 const double x = 1.0 + t * t;
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(kJacThreads)
                 y = y * (1.5 - 0.5 * x * y * y);
                 c = y;
                 s = t * y;
-                atomicAdd(&rot_count, 1);
+                rot_count = 1;  // benign race: every writer stores 1 (a shared atomic here serialised the round)
               }
             }
             c = __shfl_sync(hmask, c, 0, 16);

@@ -1,19 +1,19 @@
 // Batched SCW (Algorithm 1) and per-matrix errors on the test stream.
 //
 // For each test matrix A_b (m x n) and sketch S (k x m):
-//   1. B   = S A_b                        (k x n)   -- Alg. 1 line 1 operand
-//   2. V^T = orthonormal basis of rowspace(B) (k x n): eigen-orthonormalisation
-//            B B^T = W diag(mu) W^T,  V^T = diag(mu^{-1/2}) W^T B  (directions with
-//            mu <= 1e-13 mu_max dropped; reading c2).  "The full SVD in line 1 is used for
-//            orthogonalization ... can be replaced" -- any orthonormal basis of the
-//            row space gives the same A_hat.
-//   3. Z^T = (A_b V)^T                     (k x m)
-//   4. Z^T Z = W2 diag(sigma^2) W2^T       (the SVD of AV, line 2, through its k x k Gram)
+//   1. B   = S A_b                        (k x n)   -- Alg. 1 line 1 operand, P:61, P:276;
+//            tcgen05 3xTF32, A_b read transposed (gemm_tc.cu, xt)
+//   2. V^T = orthonormal basis of rowspace(B) (k x n): fp64 Gram C = B B^T, pivoted Cholesky
+//            P C P^T = L L^T, V^T = L^{-1} P B (pivots <= 1e-13 max diag dropped; reading c2).
+//            "The full SVD in line 1 is used for orthogonalization ... it can be replaced with
+//            QR" -- any orthonormal basis of the row space gives the same A_hat.
+//   3. Z^T = (A_b V)^T                     (k x m)   -- tcgen05 3xTF32
+//   4. Z^T Z = W2 diag(sigma^2) W2^T       (the SVD of AV, line 2, through its k x k Gram; Jacobi)
 //   5. L = Z W2_r = U2_r diag(sigma_r) (m x r),  R = V W2_r (n x r)  =>  A_hat = [AV]_r V^T = L R^T
 //   6. e_b = ||A_b - L R^T||_F             dense residual, fp64 reduction (not the identity
 //            ||A||^2 - sum sigma^2, which cancels catastrophically)
-// Products 1, 3, 6 accumulate fp32 products on CUDA cores; small Gram / rotation steps are
-// fp64.  Everything is batched over b (grid.y / grid.z) with deterministic reductions.
+// Small Grams, factorizations and rotations are fp64.  Everything is batched over b with
+// deterministic (fixed-order) reductions.
 #include <algorithm>
 #include <cmath>
 
@@ -21,66 +21,6 @@
 #include "tsk_internal.h"
 
 namespace tsk {
-
-// ---------------------------------------------------------------- C = X X^T (rows of an fp32 k x len matrix), fp64
-// grid (ceil(npairs / (256*kPer)), batch); each thread owns kPer lower-triangle pairs (a >= c).
-constexpr int kGramPer = 8;
-__global__ void __launch_bounds__(256) gram_rows_kernel(const float* __restrict__ X, int k, int len,
-                                                        double* __restrict__ C) {
-  extern __shared__ float xs[];  // [k][65]
-  const int b = blockIdx.y;
-  const float* Xb = X + (size_t)b * k * len;
-  const int npairs = k * (k + 1) / 2;
-  double acc[kGramPer];
-  int pa[kGramPer], pc[kGramPer];
-#pragma unroll
-  for (int u = 0; u < kGramPer; ++u) {
-    acc[u] = 0.0;
-    const int e = blockIdx.x * 256 * kGramPer + u * 256 + threadIdx.x;
-    if (e < npairs) {
-      int a = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-      while ((a + 1) * (a + 2) / 2 <= e) ++a;
-      while (a * (a + 1) / 2 > e) --a;
-      pa[u] = a;
-      pc[u] = e - a * (a + 1) / 2;
-    } else {
-      pa[u] = -1;
-      pc[u] = 0;
-    }
-  }
-  for (int j0 = 0; j0 < len; j0 += 64) {
-    for (int e = threadIdx.x; e < k * 64; e += 256) {
-      const int a = e >> 6, jj = e & 63;
-      xs[a * 65 + jj] = (j0 + jj < len) ? Xb[(size_t)a * len + j0 + jj] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kGramPer; ++u) {
-      if (pa[u] >= 0) {
-        const float* ra = xs + pa[u] * 65;
-        const float* rc = xs + pc[u] * 65;
-        double s = 0.0;
-#pragma unroll 8
-        for (int jj = 0; jj < 64; ++jj) s += (double)ra[jj] * (double)rc[jj];
-        acc[u] += s;
-      }
-    }
-    __syncthreads();
-  }
-  double* Cb = C + (size_t)b * k * k;
-#pragma unroll
-  for (int u = 0; u < kGramPer; ++u)
-    if (pa[u] >= 0) {
-      Cb[(size_t)pa[u] * k + pc[u]] = acc[u];
-      Cb[(size_t)pc[u] * k + pa[u]] = acc[u];
-    }
-}
-
-static void launch_gram_rows(const float* X, int k, int len, int batch, double* C, cudaStream_t s) {
-  const int npairs = k * (k + 1) / 2;
-  dim3 g((npairs + 256 * kGramPer - 1) / (256 * kGramPer), batch);
-  gram_rows_kernel<<<g, 256, (size_t)k * 65 * 4, s>>>(X, k, len, C);
-}
 
 // ---------------------------------------------------------------- 2. V^T = diag(mu^-1/2) W^T B
 // thread per column j: its B column (k values) is cached in registers, W comes from shared memory
@@ -156,213 +96,259 @@ __global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles
   err[b] = sqrt(s);
 }
 
-// ---------------------------------------------------------------- register-tiled SIMT products
-// 256 threads compute a [CB x 128] output tile; thread (ty = tid/16, tx = tid%16) owns rows
-// ty*CT .. ty*CT+CT-1 (CT = CB/16) and columns tx + 16u (u < 8): per contraction step it reads
-// CT + 8 operands from shared memory and issues 8*CT FMAs (fp32, round-to-nearest).
-constexpr int kTK = 16;  // contraction chunk
-
-// Out[b][c][j] = sum_i P[c][i] A[b][i][j]      (B = S A: P = S [k][m], A [m][n], Out [k][n])
-template <int CB>
-__global__ void __launch_bounds__(256) scw_sa_tiled_kernel(const float* __restrict__ A, const float* __restrict__ P,
-                                                           int m, int n, int k, float* __restrict__ Out) {
-  constexpr int CT = CB / 16;
-  __shared__ float Ps[kTK][CB + 4];
-  __shared__ float As[kTK][128 + 4];
-  const int b = blockIdx.z;
-  const int c0 = blockIdx.y * CB, j0 = blockIdx.x * 128;
+// ---------------------------------------------------------------- C = X X^T, register-tiled fp64
+// grid (tiles^2, batch): CTA (ta, tc) computes the 64 x 64 block rows [64 ta, +64) x cols [64 tc, +64)
+// of C[b] (k <= 128) for X_b fp32 [k][len]; 256 threads = 16 x 16, each a 4 x 4 block.  X chunks are
+// converted to fp64 once on their way into shared memory (exact), products accumulate in fp64.
+__global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __restrict__ X, int k, int len,
+                                                              double* __restrict__ C) {
+  constexpr int KC = 32;
+  __shared__ __align__(16) double xa[KC][64];
+  __shared__ __align__(16) double xc[KC][64];
+  const int b = blockIdx.y;
+  const int nt = (k + 63) / 64;
+  const int ta = blockIdx.x / nt, tc = blockIdx.x % nt;
+  if (tc > ta) return;  // upper blocks are mirrored from the lower ones
+  const float* Xb = X + (size_t)b * k * len;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const float* Ab = A + (size_t)b * m * n;
-  float acc[CT][8];
+  double acc[4][4];
 #pragma unroll
-  for (int v = 0; v < CT; ++v)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
-  for (int i0 = 0; i0 < m; i0 += kTK) {
-    // A chunk [16][128]: 512 float4, 2 per thread (rows contiguous in j)
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      const int e = tid + w * 256;
-      const int ii = e >> 5, jq = (e & 31) * 4;
-      const int i = i0 + ii, j = j0 + jq;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < m) {
-        if (j + 3 < n) v = *reinterpret_cast<const float4*>(Ab + (size_t)i * n + j);
-        else {
-          if (j < n) v.x = Ab[(size_t)i * n + j];
-          if (j + 1 < n) v.y = Ab[(size_t)i * n + j + 1];
-          if (j + 2 < n) v.z = Ab[(size_t)i * n + j + 2];
-        }
-      }
-      *reinterpret_cast<float4*>(&As[ii][jq]) = v;
-    }
-    // P chunk [CB][16] -> Ps[16][CB]
-    for (int e = tid; e < CB * kTK; e += 256) {
-      const int c = e >> 4, ii = e & 15;
-      Ps[ii][c] = (c0 + c < k && i0 + ii < m) ? P[(size_t)(c0 + c) * m + i0 + ii] : 0.f;
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int j0 = 0; j0 < len; j0 += KC) {
+    for (int e = tid; e < 64 * KC; e += 256) {
+      // consecutive threads: consecutive rows (conflict-free fp64 stores; the strided global reads
+      // of one 32-column chunk share sectors through L1)
+      const int r = e % 64, jj = e / 64;
+      const int ra = ta * 64 + r, rc = tc * 64 + r;
+      const bool inj = j0 + jj < len;
+      xa[jj][r] = (ra < k && inj) ? (double)Xb[(size_t)ra * len + j0 + jj] : 0.0;
+      xc[jj][r] = (rc < k && inj) ? (double)Xb[(size_t)rc * len + j0 + jj] : 0.0;
     }
     __syncthreads();
+#pragma unroll 8
+    for (int jj = 0; jj < KC; ++jj) {
+      const double2 a01 = *reinterpret_cast<const double2*>(&xa[jj][ty * 4]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&xa[jj][ty * 4 + 2]);
+      const double2 c01 = *reinterpret_cast<const double2*>(&xc[jj][tx * 4]);
+      const double2 c23 = *reinterpret_cast<const double2*>(&xc[jj][tx * 4 + 2]);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double cv[4] = {c01.x, c01.y, c23.x, c23.y};
 #pragma unroll
-    for (int ii = 0; ii < kTK; ++ii) {
-      float pv[CT], av[8];
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int v = 0; v < CT; ++v) pv[v] = Ps[ii][ty * CT + v];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) av[u] = As[ii][tx + 16 * u];
-#pragma unroll
-      for (int v = 0; v < CT; ++v)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[v][u] = fmaf(pv[v], av[u], acc[v][u]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], cv[j], acc[i][j]);
     }
     __syncthreads();
   }
-  float* Ob = Out + (size_t)b * k * n;
+  double* Cb = C + (size_t)b * k * k;
 #pragma unroll
-  for (int v = 0; v < CT; ++v) {
-    const int c = c0 + ty * CT + v;
-    if (c >= k) continue;
+  for (int i = 0; i < 4; ++i) {
+    const int ra = ta * 64 + ty * 4 + i;
+    if (ra >= k) continue;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int j = j0 + tx + 16 * u;
-      if (j < n) Ob[(size_t)c * n + j] = acc[v][u];
+    for (int j = 0; j < 4; ++j) {
+      const int rc = tc * 64 + tx * 4 + j;
+      if (rc >= k) continue;
+      Cb[(size_t)ra * k + rc] = acc[i][j];
+      Cb[(size_t)rc * k + ra] = acc[i][j];
     }
   }
 }
 
-// Out[b][c][i] = sum_j P[b][c][j] A[b][i][j]    (Z^T = V^T A^T: P = V^T [k][n], A [m][n], Out [k][m])
-template <int CB>
-__global__ void __launch_bounds__(256) scw_av_tiled_kernel(const float* __restrict__ A, const float* __restrict__ P,
-                                                           int m, int n, int k, float* __restrict__ Out) {
-  constexpr int CT = CB / 16;
-  __shared__ float Ps[kTK][CB + 4];
-  __shared__ float As[kTK][128 + 4];
-  const int b = blockIdx.z;
-  const int c0 = blockIdx.y * CB, i0 = blockIdx.x * 128;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const float* Ab = A + (size_t)b * m * n;
-  const float* Pb = P + (size_t)b * k * n;
-  float acc[CT][8];
-#pragma unroll
-  for (int v = 0; v < CT; ++v)
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
-  for (int j0 = 0; j0 < n; j0 += kTK) {
-    // A chunk rows i0..i0+127, cols j0..j0+15 -> As[jj][i]: 512 float4, 2 per thread
-#pragma unroll
-    for (int w = 0; w < 2; ++w) {
-      const int e = tid + w * 256;
-      const int il = e >> 2, jq = (e & 3) * 4;
-      const int i = i0 + il, j = j0 + jq;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < m) {
-        if (j + 3 < n) v = *reinterpret_cast<const float4*>(Ab + (size_t)i * n + j);
-        else {
-          if (j < n) v.x = Ab[(size_t)i * n + j];
-          if (j + 1 < n) v.y = Ab[(size_t)i * n + j + 1];
-          if (j + 2 < n) v.z = Ab[(size_t)i * n + j + 2];
-        }
-      }
-      As[jq][il] = v.x;
-      As[jq + 1][il] = v.y;
-      As[jq + 2][il] = v.z;
-      As[jq + 3][il] = v.w;
-    }
-    for (int e = tid; e < CB * kTK; e += 256) {
-      const int c = e >> 4, jj = e & 15;
-      Ps[jj][c] = (c0 + c < k && j0 + jj < n) ? Pb[(size_t)(c0 + c) * n + j0 + jj] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int jj = 0; jj < kTK; ++jj) {
-      float pv[CT], av[8];
-#pragma unroll
-      for (int v = 0; v < CT; ++v) pv[v] = Ps[jj][ty * CT + v];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) av[u] = As[jj][tx + 16 * u];
-#pragma unroll
-      for (int v = 0; v < CT; ++v)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[v][u] = fmaf(pv[v], av[u], acc[v][u]);
-    }
-    __syncthreads();
-  }
-  float* Ob = Out + (size_t)b * k * m;
-#pragma unroll
-  for (int v = 0; v < CT; ++v) {
-    const int c = c0 + ty * CT + v;
-    if (c >= k) continue;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + tx + 16 * u;
-      if (i < m) Ob[(size_t)c * m + i] = acc[v][u];
-    }
-  }
+static void launch_gram_rows_tiled(const float* X, int k, int len, int batch, double* C, cudaStream_t s) {
+  const int nt = (k + 63) / 64;
+  gram_rows_tiled_kernel<<<dim3(nt * nt, batch), 256, 0, s>>>(X, k, len, C);
 }
 
-// partial[b][tile] = sum over a [64 x 128] tile of (A - L R^T)^2 ; L [m][r], R [n][r]
-__global__ void __launch_bounds__(256) scw_residual_tiled_kernel(const float* __restrict__ A,
-                                                                 const float* __restrict__ L,
-                                                                 const float* __restrict__ R, int m, int n, int r,
-                                                                 double* __restrict__ part) {
-  __shared__ float Ls[kTK][64 + 4];
-  __shared__ float Rs[kTK][128 + 4];
-  __shared__ double red[256];
+constexpr int kCholSmemMax = 220 * 1024;  // dynamic part (the kernel also has ~0.5 KB static)
+
+// ---------------------------------------------------------------- orthonormal basis by pivoted Cholesky
+// Algorithm 1 line 1 needs only an orthonormal basis of rowspace(S A) ("used for
+// orthogonalization ... can be replaced with QR").  With C = B B^T (fp64) and the pivoted
+// Cholesky P C P^T = L L^T, V^T = L^{-1} P B has orthonormal rows spanning rowspace(B).  Pivots
+// below 1e-13 of the largest diagonal end the factorisation (rank(B) < k, reading c2): the
+// remaining directions are dropped (mu = 0).  Output in the convention of scw_vt_kernel:
+// V^T[c] = sc_c sum_a W[a][c] B[a] with W[perm[i]][c] = L^{-1}[c][i], mu[c] = 1 (kept) or 0.
+__global__ void __launch_bounds__(128) chol_basis_kernel(const double* __restrict__ Cg, int k,
+                                                         double* __restrict__ W, double* __restrict__ mu) {
+  extern __shared__ double cs[];  // [k][k+1] C -> L (lower), then [k][k+1] L^{-1}
+  __shared__ int perm[128];
+  __shared__ int piv_s, rank_s;
+  __shared__ double dmax0_s;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int ld = k + 1;
+  double* L = cs;
+  double* Li = cs + (size_t)k * ld;
+  const double* Cb = Cg + (size_t)b * k * k;
+  for (int e = tid; e < k * k; e += nt) L[(e / k) * ld + e % k] = Cb[e];
+  for (int i = tid; i < k; i += nt) perm[i] = i;
+  __syncthreads();
+  if (tid == 0) {
+    double d = 0.0;
+    for (int i = 0; i < k; ++i) d = fmax(d, L[i * ld + i]);
+    dmax0_s = d;
+    rank_s = k;
+  }
+  __syncthreads();
+  const double floor_piv = 1e-13 * dmax0_s;
+  for (int j = 0; j < k; ++j) {
+    if (tid < 32) {  // pivot: largest remaining diagonal (ties -> lowest index)
+      double best = -1.0;
+      int bi = j;
+      for (int i = j + tid; i < k; i += 32) {
+        const double d = L[i * ld + i];
+        if (d > best) { best = d; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        piv_s = bi;
+        if (!(best > floor_piv)) rank_s = j;
+      }
+    }
+    __syncthreads();
+    if (rank_s == j) break;
+    const int p = piv_s;
+    if (p != j) {  // symmetric swap of rows / columns j and p (full matrix kept)
+      for (int x = tid; x < k; x += nt) {
+        const double t = L[j * ld + x];
+        L[j * ld + x] = L[p * ld + x];
+        L[p * ld + x] = t;
+      }
+      __syncthreads();
+      for (int x = tid; x < k; x += nt) {
+        const double t = L[x * ld + j];
+        L[x * ld + j] = L[x * ld + p];
+        L[x * ld + p] = t;
+      }
+      if (tid == 0) {
+        const int t = perm[j];
+        perm[j] = perm[p];
+        perm[p] = t;
+      }
+      __syncthreads();
+    }
+    const double d = sqrt(L[j * ld + j]);
+    __syncthreads();
+    for (int i = j + 1 + tid; i < k; i += nt) L[i * ld + j] /= d;
+    if (tid == 0) L[j * ld + j] = d;
+    __syncthreads();
+    // trailing update of the lower triangle (and the diagonal) of rows / cols > j
+    const int rem = k - j - 1;
+    for (int e = tid; e < rem * rem; e += nt) {
+      const int i = j + 1 + e / rem, l = j + 1 + e % rem;
+      if (l <= i) L[i * ld + l] -= L[i * ld + j] * L[l * ld + j];
+    }
+    // keep the upper part consistent for the pivot swaps of later steps
+    __syncthreads();
+    for (int e = tid; e < rem * rem; e += nt) {
+      const int i = j + 1 + e / rem, l = j + 1 + e % rem;
+      if (l > i) L[i * ld + l] = L[l * ld + i];
+    }
+    __syncthreads();
+  }
+  const int rk = rank_s;
+  // L^{-1} (rk x rk lower): thread c solves column c by forward substitution
+  for (int c = tid; c < rk; c += nt) {
+    for (int i = 0; i < c; ++i) Li[i * ld + c] = 0.0;
+    for (int i = c; i < rk; ++i) {
+      double sacc = (i == c) ? 1.0 : 0.0;
+      for (int l = c; l < i; ++l) sacc -= L[i * ld + l] * Li[l * ld + c];
+      Li[i * ld + c] = sacc / L[i * ld + i];
+    }
+  }
+  __syncthreads();
+  double* Wb = W + (size_t)b * k * k;
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, c = e % k;  // W[perm[i]][c] = Linv[c][i]
+    Wb[(size_t)perm[i] * k + c] = (c < rk && i < rk) ? Li[c * ld + i] : 0.0;
+  }
+  for (int c = tid; c < k; c += nt) mu[(size_t)b * k + c] = c < rk ? 1.0 : 0.0;
+}
+
+// partial[b][tile] = sum over a [128 x 128] tile of (A - L R^T)^2 ; L [m][r], R [n][r]
+// 256 threads = 16 x 16, each an 8 x 8 block (rows ty + 16 i, cols 4 tx + 64 h + {0..3}): L and R
+// are staged transposed in shared memory, so every contraction step is 2 + 2 float4 loads for 64
+// FMAs; the A tile is read once, coalesced (float4), and (a - s)^2 is summed in fp64.
+__global__ void __launch_bounds__(256, 2) scw_residual_tiled2_kernel(const float* __restrict__ A,
+                                                                  const float* __restrict__ L,
+                                                                  const float* __restrict__ R, int m, int n,
+                                                                  int r, double* __restrict__ part) {
+  extern __shared__ __align__(16) float rsm[];  // Lt [r][128], Rt [r][128]
+  float* Lt = rsm;
+  float* Rt = rsm + (size_t)r * 128;
+  __shared__ double red[8];
   const int b = blockIdx.z;
-  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 128;
+  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const float* Lb = L + (size_t)b * m * r;
   const float* Rb = R + (size_t)b * n * r;
-  float acc[4][8];
+  for (int e = tid; e < 128 * r; e += 256) {
+    const int row = e % 128, c = e / 128;  // conflict-free transposed stores
+    Lt[c * 128 + row] = (i0 + row < m) ? Lb[(size_t)(i0 + row) * r + c] : 0.f;
+    Rt[c * 128 + row] = (j0 + row < n) ? Rb[(size_t)(j0 + row) * r + c] : 0.f;
+  }
+  __syncthreads();
+  float acc[8][8];
 #pragma unroll
-  for (int v = 0; v < 4; ++v)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[v][u] = 0.f;
-  for (int cc0 = 0; cc0 < r; cc0 += kTK) {
-    for (int e = tid; e < 64 * kTK; e += 256) {
-      const int il = e >> 4, cc = e & 15;
-      Ls[cc][il] = (i0 + il < m && cc0 + cc < r) ? Lb[(size_t)(i0 + il) * r + cc0 + cc] : 0.f;
-    }
-    for (int e = tid; e < 128 * kTK; e += 256) {
-      const int jl = e >> 4, cc = e & 15;
-      Rs[cc][jl] = (j0 + jl < n && cc0 + cc < r) ? Rb[(size_t)(j0 + jl) * r + cc0 + cc] : 0.f;
-    }
-    __syncthreads();
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  for (int c = 0; c < r; ++c) {
+    float lv[8], rv[8];
 #pragma unroll
-    for (int cc = 0; cc < kTK; ++cc) {
-      float lv[4], rv[8];
+    for (int i = 0; i < 8; ++i) lv[i] = Lt[c * 128 + ty + 16 * i];
+    const float4 r0 = *reinterpret_cast<const float4*>(&Rt[c * 128 + tx * 4]);
+    const float4 r1 = *reinterpret_cast<const float4*>(&Rt[c * 128 + 64 + tx * 4]);
+    rv[0] = r0.x; rv[1] = r0.y; rv[2] = r0.z; rv[3] = r0.w;
+    rv[4] = r1.x; rv[5] = r1.y; rv[6] = r1.z; rv[7] = r1.w;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) lv[v] = Ls[cc][ty * 4 + v];
+    for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) rv[u] = Rs[cc][tx + 16 * u];
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[v][u] = fmaf(lv[v], rv[u], acc[v][u]);
-    }
-    __syncthreads();
+      for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(lv[i], rv[j], acc[i][j]);
   }
   const float* Ab = A + (size_t)b * m * n;
-  double s = 0.0;
+  double sacc = 0.0;
+  const bool vec = (n % 4) == 0;
 #pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    const int i = i0 + ty * 4 + v;
-    if (i >= m) continue;
+  for (int i = 0; i < 8; ++i) {
+    const int row = i0 + ty + 16 * i;
+    if (row >= m) continue;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int j = j0 + tx + 16 * u;
-      if (j < n) {
-        const double d = (double)Ab[(size_t)i * n + j] - (double)acc[v][u];
-        s += d * d;
+    for (int h = 0; h < 2; ++h) {
+      const int col = j0 + 64 * h + tx * 4;
+      float av[4];
+      if (vec && col + 3 < n) {
+        const float4 v = *reinterpret_cast<const float4*>(Ab + (size_t)row * n + col);
+        av[0] = v.x; av[1] = v.y; av[2] = v.z; av[3] = v.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) av[q] = (col + q < n) ? Ab[(size_t)row * n + col + q] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (col + q < n) {
+          const double d = (double)av[q] - (double)acc[i][4 * h + q];
+          sacc += d * d;
+        }
       }
     }
   }
-  red[tid] = s;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = sacc;
   __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (tid < o) red[tid] += red[tid + o];
-    __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[(size_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = t;
   }
-  if (tid == 0) part[(size_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = red[0];
 }
 
 static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -378,7 +364,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   float* Vt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
   float* Zt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
   double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW_3, chunk * (4 * kk + 2 * k) * 8));
-  const int tiles = (int)(nb(n, 128) * nb(m, 64));
+  const int tiles = (int)(nb(n, 128) * nb(m, 128));
   float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * r * 4));
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
   if (!Bm || !Vt || !Zt || !small || !Lw || !part) return TSK_ENOMEM;
@@ -394,24 +380,53 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     cudaFuncSetAttribute(scw_vt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
+    cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 128 * 4);
     attr = true;
   }
   tsk_status st;
   for (long long b0 = 0; b0 < B; b0 += chunk) {
     const int bc = (int)std::min(chunk, B - b0);
     const float* Ac = A + (size_t)b0 * m * n;
-    // 1. B = S A
-    if (k <= 32) scw_sa_tiled_kernel<32><<<dim3(nb(n, 128), 1, bc), 256, 0, s>>>(Ac, S, m, n, k, Bm);
-    else if (k <= 64) scw_sa_tiled_kernel<64><<<dim3(nb(n, 128), 1, bc), 256, 0, s>>>(Ac, S, m, n, k, Bm);
-    else scw_sa_tiled_kernel<64><<<dim3(nb(n, 128), nb(k, 64), bc), 256, 0, s>>>(Ac, S, m, n, k, Bm);
-    // 2. orthonormal row basis of B
-    launch_gram_rows(Bm, k, n, bc, Cb, s);
-    ctx->count_launch(2);
-    // rotation threshold 1e-10: V V^T - I is bounded by it (exactly orthogonal rotations), far below
-    // what the 1e-4 SCW-error parity needs, and it saves ~40% of the sweeps of 1e-13
-    if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) return st;
+    // 1. B = S A on tcgen05 (3xTF32): (S A_b)^T = A_b^T S^T with X = A_b read transposed (the
+    // contraction runs over the rows of A_b), Y = S broadcast to every matrix; one unit per
+    // (matrix, 128-column tile of A_b), stored transposed as B [k][n]
+    {
+      GemmProblem gp;
+      gp.X = Ac;
+      gp.Y = S;
+      gp.M = n;
+      gp.N = k;
+      gp.n = m;
+      gp.D = bc;
+      gp.xt = 1;
+      gp.x_row_stride = n;
+      gp.x_slice_stride = (long long)m * n;
+      gp.ybc = 1;
+      gp.y_row_stride = m;
+      gp.y_slice_stride = m;
+      gp.batch = 1;
+      gp.bn = k <= 64 ? 64 : 128;
+      gp.dout = Bm;
+      gp.dstride = (long long)k * n;
+      gp.ldd = n;
+      if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
+    }
+    // 2. orthonormal row basis of B: fp64 Gram, pivoted Cholesky, V^T = L^{-1} P B (k > 116 does
+    // not fit the factor and its inverse in shared memory: eigen-orthonormalisation instead)
+    launch_gram_rows_tiled(Bm, k, n, bc, Cb, s);
+    ctx->count_launch(1);
+    if ((st = launch_status("scw gram(SA)")) != TSK_OK) return st;
+    if ((size_t)2 * k * (k + 1) * 8 <= (size_t)kCholSmemMax) {
+      chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cb, k, Wc, mu);
+      ctx->count_launch(1);
+      if ((st = launch_status("scw chol_basis")) != TSK_OK) return st;
+    } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) {
+      return st;
+    }
     if (k <= 64) scw_vt_kernel<64><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
     else scw_vt_kernel<128><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
+    if ((st = launch_status("scw vt")) != TSK_OK) return st;
     // 3. Z^T = V^T A^T
     {
       // Z^T[b] = V^T[b] A[b]^T on tcgen05 (3xTF32): X = A_b (m rows, K = n), Y = V^T_b (k rows),
@@ -435,8 +450,9 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
     }
     // 4. SVD of AV through its Gram
-    launch_gram_rows(Zt, k, m, bc, H, s);
-    ctx->count_launch(3);
+    launch_gram_rows_tiled(Zt, k, m, bc, H, s);
+    ctx->count_launch(1);
+    if ((st = launch_status("scw gram(AV)")) != TSK_OK) return st;
     if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10)) != TSK_OK) return st;
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
@@ -455,12 +471,13 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     }
     // 6. dense residual
     if (err) {
-      dim3 gres(nb(n, 128), nb(m, 64), bc);
-      scw_residual_tiled_kernel<<<gres, 256, 0, s>>>(Ac, Lc, Rc, m, n, r, part);
+      dim3 gres(nb(n, 128), nb(m, 128), bc);
+      scw_residual_tiled2_kernel<<<gres, 256, (size_t)2 * r * 128 * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
+      if ((st = launch_status("scw residual")) != TSK_OK) return st;
       scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
       ctx->count_launch(2);
     }
-    if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
+    if ((st = launch_status("scw")) != TSK_OK) return st;
   }
   return TSK_OK;
 }

@@ -4,12 +4,22 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/tsketch.h"
 
 struct tsk_ctx_s;
 
 namespace tsk {
+
+// launch check: TSK_ECUDA on a launch error, with the CUDA message on stderr when TSK_DEBUG is set
+inline tsk_status launch_status(const char* where) {
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e == cudaSuccess) return TSK_OK;
+  if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] %s: %s\n", where, cudaGetErrorString(e));
+  return TSK_ECUDA;
+}
 
 enum WorkspaceId {
   WS_GEMM_PARTIAL = 0,
@@ -110,6 +120,8 @@ struct GemmProblem {
   int spin_waits = 0;  // pair Gram: mbarrier waits without a suspend-time hint (diagnostics)
   int one_cta = 0;  // 1: symmetric Gram on the 1-CTA TS kernel instead of CTA pairs (diagnostics)
   int batch = 0;          // 1: D independent problems (no contraction over slices)
+  int xt = 0;             // 1: X_z stored transposed, [K = n][M] with M contiguous (x_row_stride = K stride)
+  int ybc = 0;            // 1: Y broadcast (slice 0 for every z; TS kernel only)
   int bn = 128;           // MMA N tile: 128 or 64
   float* dout = nullptr;  // direct fp32 output, transposed: dout[b * dstride + col * ldd + row]
   long long dstride = 0;
