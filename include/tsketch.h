@@ -26,8 +26,8 @@
  * - Errors: argument errors return synchronously and enqueue nothing.  Device faults surface
  *   as TSK_ECUDA on this or a later call (or tsk_sync).
  * - Threading: one ctx per host thread/stream; different ctxs are independent.
- * - Determinism: fixed reduction orders, no floating-point atomics: identical inputs give
- *   bit-identical outputs.
+ * - Determinism: fixed reduction orders (fp64 partial sums are reduced at L2 by a single thread
+ *   per address, in program order): identical inputs give bit-identical outputs.
  */
 #ifndef TSKETCH_H_
 #define TSKETCH_H_
@@ -121,6 +121,50 @@ tsk_status sketch_apply_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n
 tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
                      double* err);
 
+/* ---------------------------------------------------------------------- two-sided variant */
+/* the paper's second algorithm (Section 3.2).  The
+   two-sided entry points take DEVICE pointers only (TSK_EINVAL for host memory). */
+
+/* Mode-2 Gram (the HOSVD initial factor of Algorithm 5 along mode 2):
+     G2 (+)= sum_{d<D} A_d^T A_d          A: [D][m][n] fp32 (m % 4 == 0);  G64: [n][n] fp64
+   3xTF32 tensor cores with both operands read transposed (the contraction runs over the rows of
+   every A_d), lower-triangle tiles, mirrored (exactly symmetric). */
+tsk_status sketch_gram_mode2(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int accumulate);
+
+typedef struct {
+  int max_sweeps;    /* HOOI sweeps cap; default (<= 0): 10 */
+  double rel_tol;    /* stop when |res_{s-1} - res_s| <= rel_tol * res_{s-1}; default 1e-6 */
+} tsk_hooi_opts;
+
+typedef struct {
+  int sweeps;                   /* sweeps run */
+  int converged;                /* rel_tol reached */
+  double a_fro2;                /* ||A||_F^2 of the training tensor (trace of the mode-1 Gram) */
+  double residual_history[65];  /* [0]: HOSVD init, [s]: after sweep s (||A - G x1 S^T x2 W^T||_F) */
+} tsk_hooi_info;
+
+/* Tucker2 of the training tensor by HOOI over modes 1-2 (Eq. (9); Algorithm 5,
+   PAPER.md:446-473; readings t1-t4 in DESIGN.md): HOSVD init S <- top-k eigenvectors of
+   sum A_d A_d^T, W <- top-l of sum A_d^T A_d; each sweep
+     mode 1: Y_d = A_d W^T (m x l), S <- top-k eigenvectors of sum_d Y_d Y_d^T
+     mode 2: Z_d = A_d^T S^T (n x k), W <- top-l eigenvectors of sum_d Z_d Z_d^T
+   (the truncated SVDs of the projected unfoldings, through their Grams).  S [k][m], W [l][n]
+   fp32 with orthonormal rows (sign rule c5).  1 <= k <= m, 1 <= l <= n, m % 4 == n % 4 == 0. */
+tsk_status sketch_train_two_sided(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, int l, float* S,
+                                  float* W, const tsk_hooi_opts* opts, tsk_hooi_info* info);
+
+/* Two-sided SCW (Algorithm 3) on B test matrices A [B][m][n] with S [k][m] and
+   W [l][n]: Q = orthonormal basis of rowspace(S A_b), P = orthonormal basis of col(A_b W^T),
+   A_hat_b = P [P^T A_b Q]_r Q^T = L_b R_b^T,  L [B][m][r], R [B][n][r] (orthonormal columns),
+   sigma [B][r] the singular values of P^T A_b Q.  Any of L, R, sigma may be NULL.
+   r > min(k, l) is clamped (TSK_WARN_RANK_CLAMPED). */
+tsk_status sketch_apply_two_sided_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
+                                      const float* W, int l, int r, float* L, float* R, float* sigma);
+
+/* err[b] = ||A_b - two-sided SCW(A_b, S, W, r)||_F (fp64 dense residual), err [B] fp64 device. */
+tsk_status two_sided_scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
+                               const float* W, int l, int r, double* err);
+
 /* ---------------------------------------------------------------------- diagnostics */
 
 /* Diagnostic entry to the Gram kernel (tests / microbenchmarks only; not part of the method):
@@ -129,6 +173,8 @@ tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const
      mode bit 1: issue only the H*H^T product (1xTF32),
      mode bit 2: disable the drift throttle between units sharing a K window,
      mode bit 3: use the SS kernel variant (A operand from shared memory instead of TMEM),
+     mode bit 4: use the 1-CTA TS kernel instead of the CTA-pair kernel,
+     mode bit 5: CTA-pair kernel with mbarrier waits that spin without a suspend-time hint,
    chain / splits as in tsk_train_opts (0 = default). */
 tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int mode, int chain,
                           int splits);

@@ -30,7 +30,9 @@ STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVER
 
 # every symbol include/tsketch.h declares (checked by tests/test_abi.py on CPU)
 EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_status_string", "tsk_launch_count",
-            "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "tsk_gram_probe", "tsk_eig_probe"]
+            "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2",
+            "sketch_train_two_sided", "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe",
+            "tsk_eig_probe"]
 
 
 class TskError(RuntimeError):
@@ -50,6 +52,19 @@ class TrainInfo(ctypes.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class HooiOpts(ctypes.Structure):
+    _fields_ = [("max_sweeps", ctypes.c_int), ("rel_tol", ctypes.c_double)]
+
+
+class HooiInfo(ctypes.Structure):
+    _fields_ = [("sweeps", ctypes.c_int), ("converged", ctypes.c_int), ("a_fro2", ctypes.c_double),
+                ("residual_history", ctypes.c_double * 65)]
+
+    def as_dict(self):
+        return {"sweeps": self.sweeps, "converged": bool(self.converged), "a_fro2": self.a_fro2,
+                "residual_history": [self.residual_history[i] for i in range(self.sweeps + 1)]}
 
 
 _lib: Optional[ctypes.CDLL] = None
@@ -77,10 +92,16 @@ def lib() -> ctypes.CDLL:
         L.sketch_train.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, f64p, vp, vp]
         L.sketch_apply_scw.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, i32, f32p, f32p, f32p]
         L.scw_error.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, i32, f64p]
+        L.sketch_gram_mode2.argtypes = [vp, f32p, i64, i32, i32, f64p, i32]
+        L.sketch_train_two_sided.argtypes = [vp, f32p, i64, i32, i32, i32, i32, f32p, f32p, vp, vp]
+        L.sketch_apply_two_sided_scw.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, f32p, i32, i32, f32p, f32p,
+                                                 f32p]
+        L.two_sided_scw_error.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, f32p, i32, i32, f64p]
         L.tsk_gram_probe.argtypes = [vp, f32p, i64, i32, i32, f64p, i32, i32, i32]
         L.tsk_eig_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
-                  "sketch_train", "sketch_apply_scw", "scw_error", "tsk_gram_probe", "tsk_eig_probe"):
+                  "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2", "sketch_train_two_sided",
+                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -97,7 +118,8 @@ def _check(status: int, what: str) -> int:
     if status < 0:
         raise TskError(status, what)
     if status == TSK_WARN_NOT_CONVERGED:
-        warnings.warn(f"{what}: eigensolver reached max_iters (S valid, not converged)", RuntimeWarning)
+        warnings.warn(f"{what}: iteration cap reached before the convergence test passed (result valid)",
+                      RuntimeWarning)
     elif status == TSK_WARN_RANK_CLAMPED:
         warnings.warn(f"{what}: r > k, clamped to k", RuntimeWarning)
     return status
@@ -285,6 +307,65 @@ def tsk_eig_probe(H: torch.Tensor, ctx: Optional[Context] = None):
     sw = torch.empty((B,), dtype=torch.int32, device=H.device)
     _check(lib().tsk_eig_probe(ctx.handle, _ptr(H), p, B, _ptr(W), _ptr(lam), _ptr(sw)), "tsk_eig_probe")
     return W, lam, sw
+
+
+# ---------------------------------------------------------------------------- two-sided variant
+def sketch_gram_mode2(A: torch.Tensor, G64: Optional[torch.Tensor] = None, accumulate: bool = False,
+                      ctx: Optional[Context] = None) -> torch.Tensor:
+    """G2 (+)= sum_d A_d^T A_d (n x n fp64), the mode-2 Gram (HOSVD init of Algorithm 5)."""
+    _need(A, torch.float32, "A", 3)
+    D, m, n = A.shape
+    ctx = ctx or context(A.device)
+    G64 = G64 if G64 is not None else torch.empty((n, n), dtype=torch.float64, device=A.device)
+    _check(lib().sketch_gram_mode2(ctx.handle, _ptr(A), D, m, n, _ptr(G64), int(accumulate)), "sketch_gram_mode2")
+    return G64
+
+
+def sketch_train_two_sided(A: torch.Tensor, k: int, l: int, max_sweeps: int = 0, rel_tol: float = 0.0,
+                           ctx: Optional[Context] = None):
+    """Tucker2 by HOOI over modes 1-2 (Eq. (9), Algorithm 5): returns (S [k][m], W [l][n], info dict, status)."""
+    _need(A, torch.float32, "A", 3)
+    D, m, n = A.shape
+    ctx = ctx or context(A.device)
+    S = torch.empty((k, m), dtype=torch.float32, device=A.device)
+    W = torch.empty((l, n), dtype=torch.float32, device=A.device)
+    o = HooiOpts(max_sweeps, rel_tol)
+    info = HooiInfo()
+    st = _check(lib().sketch_train_two_sided(ctx.handle, _ptr(A), D, m, n, k, l, _ptr(S), _ptr(W), ctypes.byref(o),
+                                             ctypes.byref(info)), "sketch_train_two_sided")
+    return S, W, info.as_dict(), st
+
+
+def sketch_apply_two_sided_scw(A: torch.Tensor, S: torch.Tensor, W: torch.Tensor, r: int,
+                               ctx: Optional[Context] = None):
+    """Algorithm 3: A_hat_b = L_b R_b^T; returns (L [B][m][r], R [B][n][r], sigma [B][r])."""
+    _need(A, torch.float32, "A", 3)
+    _need(S, torch.float32, "S", 2)
+    _need(W, torch.float32, "W", 2)
+    B, m, n = A.shape
+    k, l = S.shape[0], W.shape[0]
+    rr = min(r, k, l)
+    ctx = ctx or context(A.device)
+    L = _alloc((B, m, rr), torch.float32, A)
+    R = _alloc((B, n, rr), torch.float32, A)
+    sig = _alloc((B, rr), torch.float32, A)
+    _check(lib().sketch_apply_two_sided_scw(ctx.handle, _ptr(A), B, m, n, _ptr(S), k, _ptr(W), l, r, _ptr(L),
+                                            _ptr(R), _ptr(sig)), "sketch_apply_two_sided_scw")
+    return L, R, sig
+
+
+def two_sided_scw_error(A: torch.Tensor, S: torch.Tensor, W: torch.Tensor, r: int,
+                        ctx: Optional[Context] = None) -> torch.Tensor:
+    """err[b] = ||A_b - two-sided SCW(A_b, S, W, r)||_F (fp64, dense residual)."""
+    _need(A, torch.float32, "A", 3)
+    _need(S, torch.float32, "S", 2)
+    _need(W, torch.float32, "W", 2)
+    B, m, n = A.shape
+    ctx = ctx or context(A.device)
+    err = _alloc((B,), torch.float64, A)
+    _check(lib().two_sided_scw_error(ctx.handle, _ptr(A), B, m, n, _ptr(S), S.shape[0], _ptr(W), W.shape[0], r,
+                                     _ptr(err)), "two_sided_scw_error")
+    return err
 
 
 from .dist import shard_range, train  # noqa: E402,F401

@@ -429,6 +429,63 @@ tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const
   return scw_common(ctx, A, B, m, n, S, k, r, nullptr, nullptr, nullptr, err);
 }
 
+// ------------------------------------------------------------------------------ two-sided variant
+// (device pointers only)
+tsk_status sketch_gram_mode2(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int accumulate) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !G64) return TSK_ENULL;
+  if (D < 1 || m < 1 || n < 1) return TSK_EINVAL;
+  if ((m % 4) || (n % 4)) return TSK_ESHAPE;
+  if (!is_device_ptr(A) || !is_device_ptr(G64)) return TSK_EINVAL;
+  cudaSetDevice(ctx->c.device);
+  return tsk::gram_mode2(&ctx->c, A, D, m, n, G64, accumulate);
+}
+
+tsk_status sketch_train_two_sided(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, int l, float* S,
+                                  float* W, const tsk_hooi_opts* opts, tsk_hooi_info* info) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !S || !W) return TSK_ENULL;
+  if (D < 1 || m < 1 || n < 1 || k < 1 || k > m || l < 1 || l > n) return TSK_EINVAL;
+  if ((m % 4) || (n % 4)) return TSK_ESHAPE;
+  if ((m > 256 && k + 16 > 256) || (n > 256 && l + 16 > 256)) return TSK_EINVAL;
+  if (!is_device_ptr(A) || !is_device_ptr(S) || !is_device_ptr(W)) return TSK_EINVAL;
+  cudaSetDevice(ctx->c.device);
+  return tsk::hooi_tucker2(&ctx->c, A, D, m, n, k, l, S, W, opts, info);
+}
+
+static tsk_status scw2_common(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
+                              const float* W, int l, int r, float* L, float* R, float* sigma, double* err) {
+  if (!ctx) return TSK_ENULL;
+  if (B < 0 || m < 1 || n < 1 || k < 1 || k > m || l < 1 || l > n || r < 1) return TSK_EINVAL;
+  if (B > 0 && (!A || !S || !W)) return TSK_ENULL;
+  if ((m % 4) || (n % 4)) return TSK_ESHAPE;
+  if (k > 116 || l > 116) return TSK_EINVAL;
+  tsk_status warn = TSK_OK;
+  if (r > std::min(k, l)) {
+    r = std::min(k, l);
+    warn = TSK_WARN_RANK_CLAMPED;
+  }
+  if (r > std::min(m, n) || r > 64) return TSK_EINVAL;
+  if (B == 0) return warn;
+  if (!is_device_ptr(A) || !is_device_ptr(S) || !is_device_ptr(W) || (L && !is_device_ptr(L)) ||
+      (R && !is_device_ptr(R)) || (sigma && !is_device_ptr(sigma)) || (err && !is_device_ptr(err)))
+    return TSK_EINVAL;
+  cudaSetDevice(ctx->c.device);
+  tsk_status s = tsk::scw2_run(&ctx->c, A, B, m, n, S, k, W, l, r, L, R, sigma, err);
+  return is_error(s) ? s : warn;
+}
+
+tsk_status sketch_apply_two_sided_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
+                                      const float* W, int l, int r, float* L, float* R, float* sigma) {
+  return scw2_common(ctx, A, B, m, n, S, k, W, l, r, L, R, sigma, nullptr);
+}
+
+tsk_status two_sided_scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
+                               const float* W, int l, int r, double* err) {
+  if (B > 0 && !err) return TSK_ENULL;
+  return scw2_common(ctx, A, B, m, n, S, k, W, l, r, nullptr, nullptr, nullptr, err);
+}
+
 tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int mode, int chain,
                           int splits) {
   if (!ctx) return TSK_ENULL;

@@ -62,6 +62,7 @@ struct GemmArgs {
   float* dout;   // direct fp32 output, transposed: dout[b * dstride + col * ldd + row] (requires S == 1)
   int xt;        // X operand stored transposed ([z][K][M], M contiguous): the transform reads tile columns
   int ybc;       // Y broadcast: every slice z uses Y slice 0
+  int drow;      // direct output row-major: dout[b * dstride + row * ldd + col]
   long long dstride;
   int ldd;
 };
@@ -368,18 +369,22 @@ constexpr int kTsSmemBytes = (kRawStages * 2 + kTsLoStages) * kTileBytes + 1024 
 constexpr uint32_t kTsAccCols = 128;
 constexpr uint32_t kTsAStageCols = 64;
 
-template <bool kN64>
+// kYT: the Y operand is stored transposed ([z][K][N], N contiguous); the transform then writes
+// both H_Y and L_Y in the swizzled K-major layout (the lo ring holds both, the raw ring shrinks).
+template <bool kN64, bool kYT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                           const GemmArgs a) {
+  constexpr int RS = kYT ? kRawStages - 1 : kRawStages;   // raw ring depth
+  constexpr int LB = kYT ? 2 * kTileBytes : kTileBytes;   // lo stage: [L_Y] or [H_Y | L_Y]
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* raw_base = smem;                                 // [kRawStages][X|Y]
-  uint8_t* lo_base = smem + kRawStages * 2 * kTileBytes;    // [kTsLoStages][L_Y]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lo_base + kTsLoStages * kTileBytes);
+  uint8_t* raw_base = smem;                                 // [RS][X|Y]
+  uint8_t* lo_base = smem + RS * 2 * kTileBytes;            // [kTsLoStages][LB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lo_base + kTsLoStages * LB);
   uint64_t* rfull = bars;
-  uint64_t* rempty = rfull + kRawStages;
-  uint64_t* lfull = rempty + kRawStages;
+  uint64_t* rempty = rfull + RS;
+  uint64_t* lfull = rempty + RS;
   uint64_t* lempty = lfull + kTsLoStages;
   uint64_t* accf = lempty + kTsLoStages;
   uint64_t* acce = accf + 2;
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&mapX);
     tma_prefetch_desc(&mapY);
-    for (int i = 0; i < kRawStages; ++i) {
+    for (int i = 0; i < RS; ++i) {
       mbar_init(&rfull[i], 1);
       mbar_init(&rempty[i], 1);
     }
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto raw_ptr = [&](int st, int which) { return raw_base + (st * 2 + which) * kTileBytes; };
-  auto lo_ptr = [&](int st) { return lo_base + st * kTileBytes; };
+  auto lo_ptr = [&](int st) { return lo_base + st * LB; };
 
   if (warp == 0) {
     // ===================== TMA producer + drift throttle (as in the SS kernel) =====================
@@ -429,14 +434,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (long long q = q0; q < q1; ++q) {
         if (lane == 0) {
           mbar_wait(&rempty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&rfull[st], diag ? kTileBytes : 2 * kTileBytes);
+          const uint32_t ybytes = kYT ? (uint32_t)(a.bn * kBK * 4) : (uint32_t)kTileBytes;
+          mbar_arrive_expect_tx(&rfull[st], diag ? (uint32_t)kTileBytes : (uint32_t)kTileBytes + ybytes);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
           if (a.xt) tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], bi * kBM, kc, z);  // box {128 M, 32 K}
           else tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
-          if (!diag) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * a.bn, a.ybc ? 0 : z);
+          if (!diag) {
+            if (kYT) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], bj * a.bn, kc, a.ybc ? 0 : z);  // box {bn N, 32 K}
+            else tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * a.bn, a.ybc ? 0 : z);
+          }
         }
-        if (++st == kRawStages) { st = 0; ph ^= 1; }
+        if (++st == RS) { st = 0; ph ^= 1; }
         const unsigned done = (unsigned)(q - q0 + 1);
         if (a.lag > 0 && ((done & 31u) == 0 || q + 1 == q1)) {
           if (lane == 0) st_volatile_u32(&a.progress[u], q + 1 == q1 ? 0xFFFFFFFFu : done);
@@ -485,8 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t dx = kN64 ? d + 64 : d;
           const uint32_t a_hi = tmem_base + 2 * kTsAccCols + (uint32_t)ls * kTsAStageCols;
           const uint32_t a_lo = a_hi + 32;
-          const uint64_t yh = sw128_kmajor_desc(smem_u32(raw_ptr(rs, diag ? 0 : 1)));
-          const uint64_t yl = sw128_kmajor_desc(smem_u32(lo_ptr(ls)));
+          const uint64_t yh = kYT ? sw128_kmajor_desc(smem_u32(lo_ptr(ls)))
+                                  : sw128_kmajor_desc(smem_u32(raw_ptr(rs, diag ? 0 : 1)));
+          const uint64_t yl = sw128_kmajor_desc(smem_u32(lo_ptr(ls)) + (kYT ? (uint32_t)kTileBytes : 0u));
 #pragma unroll
           for (int kk = 0; kk < kBK / 8; ++kk) {
             const uint64_t adv = (uint64_t)(kk * 32 >> 4);  // +32 B per K=8 step inside the swizzle atom
@@ -496,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_tf32_ts(dx, a_lo + kk * 8, yh + adv, idesc, 1u);
           }
           mma_commit(&rempty[rs]);
-          if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+          if (++rs == RS) { rs = 0; rph ^= 1; }
           mma_commit(&lempty[ls]);
           if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
           if (++cpos == a.chain || q + 1 == q1) {
@@ -554,8 +564,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_32x32b_x32(ta, hi);
           tmem_st_32x32b_x32(ta + 32, lo);
         }
-        // (2) the B-side lo part: L_Y (or L_X for a diagonal tile) in the swizzled smem layout
-        {
+        // (2) the B-side lo part: L_Y (or L_X for a diagonal tile) in the swizzled smem layout; for
+        // a transposed Y, row tt of Y is column tt of the raw [32 K][bn N] tile and both H_Y and
+        // L_Y are written (row tt of the swizzled K-major tiles: 16-B chunk c at c ^ (tt & 7))
+        if (kYT) {
+          if (tt < a.bn) {
+            const float* ycol = reinterpret_cast<const float*>(raw_ptr(rs, diag ? 0 : 1)) + tt;
+            const int ys = diag ? kBM : a.bn;  // row pitch (floats) of the raw tile
+            const uint32_t hrow = smem_u32(lo_ptr(ls)) + (uint32_t)tt * 128u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              float4 h, l;
+              float* hv = &h.x;
+              float* lv = &l.x;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float e = ycol[(c * 4 + j) * ys];
+                const float hh = __uint_as_float(__float_as_uint(e) & 0xFFFFE000u);
+                hv[j] = hh;
+                lv[j] = e - hh;
+              }
+              const uint32_t off = (uint32_t)((c ^ (tt & 7)) * 16);
+              sts_f4(hrow + off, h);
+              sts_f4(hrow + (uint32_t)kTileBytes + off, l);
+            }
+          }
+        } else {
           const uint32_t src = smem_u32(raw_ptr(rs, diag ? 0 : 1));
           const uint32_t dst = smem_u32(lo_ptr(ls));
 #pragma unroll
@@ -575,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&lfull[ls]);
-        if (++rs == kRawStages) { rs = 0; rph ^= 1; }
+        if (++rs == RS) { rs = 0; rph ^= 1; }
         if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
       }
     }
@@ -660,10 +694,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int gr = bi * kBM + row;
         float* ob = a.dout + (size_t)b * a.dstride;
         if (gr < a.Mv) {
+          if (a.drow) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            const int gc = bj * a.bn + col0 + i;
-            if (col0 + i < a.bn && gc < a.Nv) ob[(size_t)gc * a.ldd + gr] = sum[i];
+            for (int i = 0; i < 64; ++i) {
+              const int gc = bj * a.bn + col0 + i;
+              if (col0 + i < a.bn && gc < a.Nv) ob[(size_t)gr * a.ldd + gc] = sum[i];
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+              const int gc = bj * a.bn + col0 + i;
+              if (col0 + i < a.bn && gc < a.Nv) ob[(size_t)gc * a.ldd + gr] = sum[i];
+            }
           }
         }
       }
@@ -756,12 +798,12 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
     return TSK_ESHAPE;
   if (p.sym && (p.X != p.Y || p.M != p.N)) return TSK_EINVAL;
   // production symmetric Gram: CTA pairs (gram_pair.cu)
-  if (p.sym && p.products == 3 && !p.raw && !p.ss && !p.one_cta && !p.batch) return gram_pair(ctx, p);
+  if (p.sym && p.products == 3 && !p.raw && !p.ss && !p.one_cta && !p.batch && !p.xt) return gram_pair(ctx, p);
   CUtensorMap mx, my;
   if (p.xt) {
     // transposed X: [D][K = n][M] with M contiguous (x_row_stride = stride between K rows);
     // box {128 M, 32 K}, no swizzle (the transform reads tile columns, 4-byte lanes: no conflicts)
-    if (p.sym || p.ss || p.products != 3 || p.raw || (p.x_row_stride % 4) || (p.M % 4)) return TSK_EINVAL;
+    if ((p.sym && !p.yt) || p.ss || p.products != 3 || p.raw || (p.x_row_stride % 4) || (p.M % 4)) return TSK_EINVAL;
     auto enc = get_encode_fn();
     if (!enc) return TSK_ECUDA;
     cuuint64_t dims[3] = {(cuuint64_t)p.M, (cuuint64_t)p.n, (cuuint64_t)p.D};
@@ -778,7 +820,23 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
     if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: X tensor map rejected\n");
     return TSK_ECUDA;
   }
-  if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) {
+  if (p.yt) {
+    // transposed Y: [D][K = n][N] with N contiguous; box {bn N, 32 K}, no swizzle
+    if (p.ss || p.products != 3 || p.raw || (p.y_row_stride % 4) || (p.N % 4)) return TSK_EINVAL;
+    auto enc = get_encode_fn();
+    if (!enc) return TSK_ECUDA;
+    const int bnv = (p.bn == 64 && !p.sym) ? 64 : 128;
+    cuuint64_t dims[3] = {(cuuint64_t)p.N, (cuuint64_t)p.n, (cuuint64_t)p.D};
+    cuuint64_t strides[2] = {(cuuint64_t)(p.y_row_stride * 4), (cuuint64_t)(p.y_slice_stride * 4)};
+    cuuint32_t box[3] = {(cuuint32_t)bnv, (cuuint32_t)kBK, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p.Y), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: transposed Y tensor map rejected\n");
+      return TSK_ECUDA;
+    }
+  } else if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) {
     if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: Y tensor map rejected\n");
     return TSK_ECUDA;
   }
@@ -808,6 +866,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.Nv = p.N;
   a.xt = p.xt;
   a.ybc = p.ybc;
+  a.drow = p.drow;
   a.dout = p.dout;
   a.dstride = p.dstride;
   a.ldd = p.ldd;
@@ -826,26 +885,37 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.progress = prog;
   if (cudaMemsetAsync(prog, 0, (size_t)a.U * sizeof(unsigned), ctx->stream) != cudaSuccess) return TSK_ECUDA;
 
+  constexpr int kTsYtSmemBytes = ((kRawStages - 1) * 2 + 2 * kTsLoStages) * kTileBytes + 1024 + 256;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
             cudaSuccess ||
-        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kTsSmemBytes) != cudaSuccess ||
-        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kTsSmemBytes) != cudaSuccess)
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTsSmemBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTsYtSmemBytes) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTsYtSmemBytes) != cudaSuccess)
       return TSK_ECUDA;
     attr_set = true;
   }
   const int grid = std::min(a.U, ctx->num_sms);
   // production: TS variant (A operand from TMEM); the SS variant serves the diagnostic modes
   if (a.products == 3 && !a.raw && !p.ss) {
-    if (a.bn == 64)
-      gemm_tf32x3_ts_kernel<true><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
-    else
-      gemm_tf32x3_ts_kernel<false><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+    if (p.yt) {
+      if (a.bn == 64)
+        gemm_tf32x3_ts_kernel<true, true><<<grid, kThreads, kTsYtSmemBytes, ctx->stream>>>(mx, my, a);
+      else
+        gemm_tf32x3_ts_kernel<false, true><<<grid, kThreads, kTsYtSmemBytes, ctx->stream>>>(mx, my, a);
+    } else if (a.bn == 64) {
+      gemm_tf32x3_ts_kernel<true, false><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+    } else {
+      gemm_tf32x3_ts_kernel<false, false><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+    }
   } else {
-    if (a.batch || a.bn != 128 || a.dout) return TSK_EINVAL;  // diagnostic SS kernel: plain problems only
+    if (a.batch || a.bn != 128 || a.dout || p.xt || p.yt) return TSK_EINVAL;  // diagnostic SS kernel: plain problems only
     gemm_tf32x3_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(mx, my, a);
   }
   if (launch_status("gemm_tf32x3") != TSK_OK) return TSK_ECUDA;

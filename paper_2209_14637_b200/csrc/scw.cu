@@ -56,13 +56,15 @@ __global__ void __launch_bounds__(128) scw_vt_kernel(const float* __restrict__ B
 }
 
 // ---------------------------------------------------------------- 5. out[i][c] = sum_a In[a][i] W[a][c], c < r
+// coefficient matrix of matrix b: W + b * wst, row stride ldw (W[a][c] at a * ldw + c)
 template <int KMAX>
 __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
-                                                          int k, int len, int r, float* __restrict__ Out) {
+                                                          int k, int len, int r, int ldw, long long wst,
+                                                          float* __restrict__ Out) {
   extern __shared__ double wsm[];  // [k][r]
   const int b = blockIdx.y;
-  const double* Wb = W + (size_t)b * k * k;
-  for (int e = threadIdx.x; e < k * r; e += blockDim.x) wsm[e] = Wb[(size_t)(e / r) * k + (e % r)];
+  const double* Wb = W + (size_t)b * wst;
+  for (int e = threadIdx.x; e < k * r; e += blockDim.x) wsm[e] = Wb[(size_t)(e / r) * ldw + (e % r)];
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= len) return;
@@ -100,16 +102,21 @@ __global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles
 // grid (tiles^2, batch): CTA (ta, tc) computes the 64 x 64 block rows [64 ta, +64) x cols [64 tc, +64)
 // of C[b] (k <= 128) for X_b fp32 [k][len]; 256 threads = 16 x 16, each a 4 x 4 block.  X chunks are
 // converted to fp64 once on their way into shared memory (exact), products accumulate in fp64.
+// cross form (X2 != nullptr): C[b] = X_b X2_b^T (k x k2, no mirroring)
 __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __restrict__ X, int k, int len,
-                                                              double* __restrict__ C) {
+                                                              double* __restrict__ C, const float* __restrict__ X2,
+                                                              int k2) {
   constexpr int KC = 32;
   __shared__ __align__(16) double xa[KC][64];
   __shared__ __align__(16) double xc[KC][64];
   const int b = blockIdx.y;
-  const int nt = (k + 63) / 64;
-  const int ta = blockIdx.x / nt, tc = blockIdx.x % nt;
-  if (tc > ta) return;  // upper blocks are mirrored from the lower ones
+  const bool cross = X2 != nullptr;
+  const int kc = cross ? k2 : k;
+  const int ntc = (kc + 63) / 64;
+  const int ta = blockIdx.x / ntc, tc = blockIdx.x % ntc;
+  if (!cross && tc > ta) return;  // upper blocks are mirrored from the lower ones
   const float* Xb = X + (size_t)b * k * len;
+  const float* Xc = cross ? X2 + (size_t)b * k2 * len : Xb;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   double acc[4][4];
 #pragma unroll
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __res
       const int ra = ta * 64 + r, rc = tc * 64 + r;
       const bool inj = j0 + jj < len;
       xa[jj][r] = (ra < k && inj) ? (double)Xb[(size_t)ra * len + j0 + jj] : 0.0;
-      xc[jj][r] = (rc < k && inj) ? (double)Xb[(size_t)rc * len + j0 + jj] : 0.0;
+      xc[jj][r] = (rc < kc && inj) ? (double)Xc[(size_t)rc * len + j0 + jj] : 0.0;
     }
     __syncthreads();
 #pragma unroll 8
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __res
     }
     __syncthreads();
   }
-  double* Cb = C + (size_t)b * k * k;
+  double* Cb = C + (size_t)b * k * kc;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int ra = ta * 64 + ty * 4 + i;
@@ -150,16 +157,52 @@ __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __res
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int rc = tc * 64 + tx * 4 + j;
-      if (rc >= k) continue;
-      Cb[(size_t)ra * k + rc] = acc[i][j];
-      Cb[(size_t)rc * k + ra] = acc[i][j];
+      if (rc >= kc) continue;
+      Cb[(size_t)ra * kc + rc] = acc[i][j];
+      if (!cross) Cb[(size_t)rc * k + ra] = acc[i][j];
     }
   }
 }
 
 static void launch_gram_rows_tiled(const float* X, int k, int len, int batch, double* C, cudaStream_t s) {
   const int nt = (k + 63) / 64;
-  gram_rows_tiled_kernel<<<dim3(nt * nt, batch), 256, 0, s>>>(X, k, len, C);
+  gram_rows_tiled_kernel<<<dim3(nt * nt, batch), 256, 0, s>>>(X, k, len, C, nullptr, 0);
+}
+
+// C[b] = X_b X2_b^T (k x k2) for X [B][k][len], X2 [B][k2][len] fp32, fp64 products
+static void launch_gram_cross(const float* X, int k, const float* X2, int k2, int len, int batch, double* C,
+                              cudaStream_t s) {
+  gram_rows_tiled_kernel<<<dim3(((k + 63) / 64) * ((k2 + 63) / 64), batch), 256, 0, s>>>(X, k, len, C, X2, k2);
+}
+
+// H[b] = M_b^T M_b for M [B][l][k] fp64 (one CTA per matrix, thread per entry of the lower triangle)
+__global__ void gram_cols_f64_kernel(const double* __restrict__ M, int l, int k, double* __restrict__ H) {
+  const int b = blockIdx.x;
+  const double* Mb = M + (size_t)b * l * k;
+  double* Hb = H + (size_t)b * k * k;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    const int i = e / k, j = e % k;
+    if (j > i) continue;
+    double s = 0.0;
+    for (int a = 0; a < l; ++a) s += Mb[(size_t)a * k + i] * Mb[(size_t)a * k + j];
+    Hb[(size_t)i * k + j] = s;
+    Hb[(size_t)j * k + i] = s;
+  }
+}
+
+// C[b] = M_b W_b[:, :r] for M [B][l][k], W [B][k][k] (columns = eigenvectors) -> C [B][l][r]
+__global__ void small_mm_f64_kernel(const double* __restrict__ M, const double* __restrict__ W, int l, int k, int r,
+                                    double* __restrict__ C) {
+  const int b = blockIdx.x;
+  const double* Mb = M + (size_t)b * l * k;
+  const double* Wb = W + (size_t)b * k * k;
+  double* Cb = C + (size_t)b * l * r;
+  for (int e = threadIdx.x; e < l * r; e += blockDim.x) {
+    const int a = e / r, c = e % r;
+    double s = 0.0;
+    for (int x = 0; x < k; ++x) s += Mb[(size_t)a * k + x] * Wb[(size_t)x * k + c];
+    Cb[(size_t)a * r + c] = s;
+  }
 }
 
 constexpr int kCholSmemMax = 220 * 1024;  // dynamic part (the kernel also has ~0.5 KB static)
@@ -353,6 +396,19 @@ __global__ void __launch_bounds__(256, 2) scw_residual_tiled2_kernel(const float
 
 static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+static void scw_attrs() {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(scw_vt_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_vt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
+    cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 128 * 4);
+    attr = true;
+  }
+}
+
 tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, int r, float* L,
                    float* R, float* sigma, double* err) {
   if (B == 0) return TSK_OK;
@@ -374,16 +430,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   double* W2 = small + 3 * chunk * kk;
   double* mu = small + 4 * chunk * kk;
   double* sig2 = mu + chunk * k;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(scw_vt_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_vt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_combine_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_combine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
-    cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 128 * 4);
-    attr = true;
-  }
+  scw_attrs();
   tsk_status st;
   for (long long b0 = 0; b0 < B; b0 += chunk) {
     const int bc = (int)std::min(chunk, B - b0);
@@ -458,11 +505,11 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
     if (k <= 64) {
-      scw_combine_kernel<64><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, Lc);
-      scw_combine_kernel<64><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, Rc);
+      scw_combine_kernel<64><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, k, (long long)kk, Lc);
+      scw_combine_kernel<64><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k, (long long)kk, Rc);
     } else {
-      scw_combine_kernel<128><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, Lc);
-      scw_combine_kernel<128><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, Rc);
+      scw_combine_kernel<128><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, k, (long long)kk, Lc);
+      scw_combine_kernel<128><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k, (long long)kk, Rc);
     }
     ctx->count_launch(2);
     if (sigma) {
@@ -478,6 +525,129 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       ctx->count_launch(2);
     }
     if ((st = launch_status("scw")) != TSK_OK) return st;
+  }
+  return TSK_OK;
+}
+
+
+// Two-sided SCW (Algorithm 3) for a batch of test matrices:
+//   1. Q^T = orthonormal basis of rowspace(S A_b)    (k x n; as steps 1-2 of SCW)
+//   2. P^T = orthonormal basis of rowspace(W A_b^T)  (l x m) = col(A_b W^T) (line 2, QR -> CholQR)
+//   3. M   = P^T A_b Q = P^T (A_b Q)                 (l x k; A_b Q as step 3 of SCW, fp64 cross Gram)
+//   4. [M]_r through M^T M = W2 diag(sigma^2) W2^T   (k x k Jacobi)
+//   5. A_hat = P [M]_r Q^T = L R^T,  L = P (M W2_r) (m x r),  R = Q W2_r (n x r)
+//   6. e_b = ||A_b - L R^T||_F                        (dense residual, fp64 reduction)
+tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, const float* W, int l,
+                    int r, float* L, float* R, float* sigma, double* err) {
+  if (B == 0) return TSK_OK;
+  if (k > 128 || l > 128 || r > 64 || r > k || r > l) return TSK_EINVAL;
+  cudaStream_t s = ctx->stream;
+  const long long chunk = std::min<long long>(B, 256);
+  const size_t kn = (size_t)k * n, km = (size_t)k * m, kk = (size_t)k * k, lm = (size_t)l * m, ll = (size_t)l * l;
+  float* Bm = reinterpret_cast<float*>(ctx->workspace(WS_SCW_0, chunk * kn * 4));
+  float* Vt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
+  float* Zt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
+  float* Yt = reinterpret_cast<float*>(ctx->workspace(WS_SCW2_0, chunk * lm * 4));
+  float* Pt = reinterpret_cast<float*>(ctx->workspace(WS_SCW2_1, chunk * lm * 4));
+  const size_t nsmall = chunk * (2 * kk + 2 * ll + 2 * (size_t)l * k + (size_t)l * r + kk + 2 * (size_t)k + 2 * (size_t)l);
+  double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW2_2, nsmall * 8));
+  const int tiles = (int)(nb(n, 128) * nb(m, 128));
+  float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * r * 4));
+  double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
+  if (!Bm || !Vt || !Zt || !Yt || !Pt || !small || !Lw || !part) return TSK_ENOMEM;
+  double* Cq = small;                      // [k][k]
+  double* Wq = Cq + chunk * kk;            // [k][k]
+  double* Cp = Wq + chunk * kk;            // [l][l]
+  double* Wp = Cp + chunk * ll;            // [l][l]
+  double* Mx = Wp + chunk * ll;            // [l][k]
+  double* H2 = Mx + chunk * (size_t)l * k; // [k][k]
+  double* W2 = H2 + chunk * kk;            // [k][k]
+  double* CL = W2 + chunk * kk;            // [l][r]
+  double* muq = CL + chunk * (size_t)l * r;
+  double* sig2 = muq + chunk * k;
+  double* mup = sig2 + chunk * k;
+  scw_attrs();
+  if ((size_t)2 * std::max(k, l) * (std::max(k, l) + 1) * 8 > (size_t)kCholSmemMax) return TSK_EINVAL;
+  tsk_status st;
+  for (long long b0 = 0; b0 < B; b0 += chunk) {
+    const int bc = (int)std::min(chunk, B - b0);
+    const float* Ac = A + (size_t)b0 * m * n;
+    // 1. Q^T: S A_b (tcgen05, A_b transposed), fp64 Gram, pivoted Cholesky, V^T = L^-1 P B
+    {
+      GemmProblem gp;
+      gp.X = Ac; gp.Y = S; gp.M = n; gp.N = k; gp.n = m; gp.D = bc;
+      gp.xt = 1; gp.x_row_stride = n; gp.x_slice_stride = (long long)m * n;
+      gp.ybc = 1; gp.y_row_stride = m; gp.y_slice_stride = m;
+      gp.batch = 1; gp.bn = k <= 64 ? 64 : 128;
+      gp.dout = Bm; gp.dstride = (long long)k * n; gp.ldd = n;
+      if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
+    }
+    launch_gram_rows_tiled(Bm, k, n, bc, Cq, s);
+    chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cq, k, Wq, muq);
+    if (k <= 64) scw_vt_kernel<64><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, Vt);
+    else scw_vt_kernel<128><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, Vt);
+    ctx->count_launch(3);
+    if ((st = launch_status("scw2 Q")) != TSK_OK) return st;
+    // 2. P^T: W A_b^T = (A_b W^T)^T (tcgen05, W broadcast, transposed store), same orthonormalisation
+    {
+      GemmProblem gp;
+      gp.X = Ac; gp.Y = W; gp.M = m; gp.N = l; gp.n = n; gp.D = bc;
+      gp.x_row_stride = n; gp.x_slice_stride = (long long)m * n;
+      gp.ybc = 1; gp.y_row_stride = n; gp.y_slice_stride = n;
+      gp.batch = 1; gp.bn = l <= 64 ? 64 : 128;
+      gp.dout = Yt; gp.dstride = (long long)l * m; gp.ldd = m;
+      if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
+    }
+    launch_gram_rows_tiled(Yt, l, m, bc, Cp, s);
+    chol_basis_kernel<<<bc, 128, (size_t)2 * l * (l + 1) * 8, s>>>(Cp, l, Wp, mup);
+    if (l <= 64) scw_vt_kernel<64><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, Pt);
+    else scw_vt_kernel<128><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, Pt);
+    ctx->count_launch(3);
+    if ((st = launch_status("scw2 P")) != TSK_OK) return st;
+    // 3. A_b Q as Z^T = Q^T A_b^T (tcgen05), then M = P^T (A_b Q) as an fp64 cross Gram of rows
+    {
+      GemmProblem gp;
+      gp.X = Ac; gp.Y = Vt; gp.M = m; gp.N = k; gp.n = n; gp.D = bc;
+      gp.x_row_stride = n; gp.x_slice_stride = (long long)m * n;
+      gp.y_row_stride = n; gp.y_slice_stride = (long long)k * n;
+      gp.batch = 1; gp.bn = k <= 64 ? 64 : 128;
+      gp.dout = Zt; gp.dstride = (long long)k * m; gp.ldd = m;
+      if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
+    }
+    launch_gram_cross(Pt, l, Zt, k, m, bc, Mx, s);
+    // 4. [M]_r through M^T M
+    gram_cols_f64_kernel<<<bc, 256, 0, s>>>(Mx, l, k, H2);
+    ctx->count_launch(2);
+    if ((st = launch_status("scw2 M")) != TSK_OK) return st;
+    if ((st = jacobi_eig_batched(ctx, H2, k, bc, W2, sig2, nullptr, 1e-10)) != TSK_OK) return st;
+    // 5. factors: L = P (M W2_r), R = Q W2_r
+    small_mm_f64_kernel<<<bc, 256, 0, s>>>(Mx, W2, l, k, r, CL);
+    float* Lc = L ? L + (size_t)b0 * m * r : Lw;
+    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
+    if (k <= 64 && l <= 64) {
+      scw_combine_kernel<64><<<dim3(nb(m, 128), bc), 128, (size_t)l * r * 8, s>>>(Pt, CL, l, m, r, r,
+                                                                                 (long long)l * r, Lc);
+      scw_combine_kernel<64><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k,
+                                                                                 (long long)kk, Rc);
+    } else {
+      scw_combine_kernel<128><<<dim3(nb(m, 128), bc), 128, (size_t)l * r * 8, s>>>(Pt, CL, l, m, r, r,
+                                                                                  (long long)l * r, Lc);
+      scw_combine_kernel<128><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k,
+                                                                                  (long long)kk, Rc);
+    }
+    ctx->count_launch(3);
+    if (sigma) {
+      scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
+      ctx->count_launch();
+    }
+    // 6. dense residual
+    if (err) {
+      dim3 gres(nb(n, 128), nb(m, 128), bc);
+      scw_residual_tiled2_kernel<<<gres, 256, (size_t)2 * r * 128 * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
+      scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
+      ctx->count_launch(2);
+    }
+    if ((st = launch_status("scw2")) != TSK_OK) return st;
   }
   return TSK_OK;
 }

@@ -41,6 +41,14 @@ enum WorkspaceId {
   WS_JACOBI,
   WS_GEMM_PROGRESS,
   WS_GRAM_SCHED,   // pair-Gram schedule (units, tile map)
+  WS_T2_G1,        // two-sided: projected mode-1 Gram (m x m fp64)
+  WS_T2_G2,        // two-sided: projected mode-2 Gram (n x n fp64)
+  WS_T2_Y,         // two-sided: A_d W^T stack
+  WS_T2_Z,         // two-sided: A_d^T S^T stack
+  WS_T2_SMALL,
+  WS_SCW2_0,       // two-sided SCW scratch
+  WS_SCW2_1,
+  WS_SCW2_2,
   WS_COUNT
 };
 
@@ -122,6 +130,8 @@ struct GemmProblem {
   int batch = 0;          // 1: D independent problems (no contraction over slices)
   int xt = 0;             // 1: X_z stored transposed, [K = n][M] with M contiguous (x_row_stride = K stride)
   int ybc = 0;            // 1: Y broadcast (slice 0 for every z; TS kernel only)
+  int yt = 0;             // 1: Y_z stored transposed, [K = n][N] with N contiguous (y_row_stride = K stride)
+  int drow = 0;           // direct output row-major: dout[b * dstride + row * ldd + col]
   int bn = 128;           // MMA N tile: 128 or 64
   float* dout = nullptr;  // direct fp32 output, transposed: dout[b * dstride + col * ldd + row]
   long long dstride = 0;
@@ -132,6 +142,14 @@ struct GemmProblem {
 tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p);
 // symmetric Gram on CTA pairs (tcgen05 cta_group::2), gram_pair.cu
 tsk_status gram_pair(Ctx* ctx, const GemmProblem& p);
+
+// two-sided variant (tucker2.cu)
+tsk_status gram_mode2(Ctx* ctx, const float* A, long long D, int m, int n, double* G64, int accumulate);
+tsk_status hooi_tucker2(Ctx* ctx, const float* A, long long D, int m, int n, int k, int l, float* S, float* W,
+                        const tsk_hooi_opts* o, tsk_hooi_info* info);
+// two-sided SCW (Algorithm 3), scw.cu; device pointers
+tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, const float* W, int l,
+                    int r, float* L, float* R, float* sigma, double* err);
 
 // eigensolver (eig.cu)
 tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda, const tsk_train_opts* o,
