@@ -61,7 +61,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
@@ -296,14 +296,24 @@ def run_tsketch(args, c):
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # issued tensor-core work of the CTA-pair schedule (gram_pair.cu): 3 products per algorithmic
+    # product over the padded 128 x 128 / 128 x 64 pair tiles (a last block with <= 64 valid rows is
+    # always the N = 64 B side; an odd tile count adds one dummy half)
+    nbk = -(-c.m // 128)
+    narrow = (c.m - 128 * (nbk - 1)) <= 64
+    t_all = nbk * (nbk + 1) // 2
+    t_n64 = nbk if narrow else 0
+    t_n128 = t_all - t_n64
+    pairs128, pairs64 = -(-t_n128 // 2), -(-t_n64 // 2)
+    issued_area = (pairs128 * 2 * 128 * 128 + pairs64 * 2 * 128 * 64) * c.n * dloc * 2 * 3
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
                 "frac": achieved / peak_tf32, "traffic": traffic,
-                "kernel": "gemm_tf32x3_kernel (+ gemm_finalize_kernel), 3xTF32 lower-triangle Gram",
+                "kernel": "gram_pair_kernel (tcgen05 cta_group::2, 3xTF32 lower-triangle Gram) + finalize",
                 "algorithmic_flops_per_launch": alg_flops,
                 "peak_note": f"TF32 = {peak_kind} bf16 sustained {mp['bf16_tflops_sustained']} TF/s x nominal "
                              f"1.1/2.25 (B200_PROFILING.md)",
-                "issued_frac": 3 * achieved / peak_tf32 * ((-(-c.m // 128) * (-(-c.m // 128) + 1) / 2 * 128 * 128)
-                                                           / (c.m * (c.m + 1) / 2)),
+                "issued_tflops": issued_area / (gram_ms / 1e3) / 1e12,
+                "issued_frac_of_nominal_tf32": issued_area / (gram_ms / 1e3) / 1.1e15,
                 "gram_ms_per_launch": gram_ms}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
