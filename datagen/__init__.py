@@ -187,3 +187,30 @@ def generate(c: StreamConfig | str, split: str = "train", start: int = 0, stop: 
         out[i].copy_(_one(c, seed, base + d, U0, sigma, device))
     return out
 
+
+
+# ------------------------------------------------------------------ random-sketch baselines (f3)
+# Draws only (no method arithmetic): the untrained sketches the paper compares against in spirit
+# ("generated randomly from some distribution, such as Gaussian", PAPER.md:27; IVY's "sparse random
+# sign matrix" initialisation, P:74; SPEC S:257-274).  Both feed the SAME SCW kernels as the trained
+# S: Algorithm 1 only uses rowspace(S A), so S need not have orthonormal rows.
+
+def random_sign_sketch(k: int, m: int, seed: int = 0) -> torch.Tensor:
+    """[k][m] fp32 CountSketch pattern: every column has exactly one nonzero, +-1, in a uniformly
+    random row (the sparsity level is a decision, not the paper's)."""
+    if not (1 <= k <= m):
+        raise ValueError("need 1 <= k <= m")
+    g = torch.Generator().manual_seed(int(seed) * 1_000_003 + 17)
+    rows = torch.randint(0, k, (m,), generator=g)
+    signs = torch.randint(0, 2, (m,), generator=g).to(torch.float32) * 2.0 - 1.0
+    S = torch.zeros(k, m, dtype=torch.float32)
+    S[rows, torch.arange(m)] = signs
+    return S
+
+
+def random_gaussian_sketch(k: int, m: int, seed: int = 0) -> torch.Tensor:
+    """[k][m] fp32 with i.i.d. N(0, 1/k) entries."""
+    if not (1 <= k <= m):
+        raise ValueError("need 1 <= k <= m")
+    g = torch.Generator().manual_seed(int(seed) * 1_000_003 + 29)
+    return (torch.randn(k, m, generator=g, dtype=torch.float64) / math.sqrt(k)).to(torch.float32)

@@ -53,3 +53,30 @@ def test_identical_variant():
 def test_bad_range():
     with pytest.raises(ValueError):
         datagen.generate("C1", "train", 0, 21)
+
+
+def test_random_sign_sketch_pattern():
+    """one nonzero per column, values +-1, deterministic under the seed; k = 1 is
+    a single row of +-1."""
+    S = datagen.random_sign_sketch(7, 50, seed=3)
+    assert S.shape == (7, 50)
+    nz = (S != 0).sum(dim=0)
+    assert torch.all(nz == 1)
+    assert torch.all(S.abs().sum(dim=0) == 1)
+    assert torch.equal(S, datagen.random_sign_sketch(7, 50, seed=3))
+    assert not torch.equal(S, datagen.random_sign_sketch(7, 50, seed=4))
+    S1 = datagen.random_sign_sketch(1, 9, seed=0)
+    assert torch.all(S1.abs() == 1)
+
+
+def test_random_gaussian_sketch_moments():
+    """determinism; mean ~ 0 within 5 standard errors at k*m = 1e4; E||Sx||^2 ~ ||x||^2
+    within 20% (JL expectation) for unit x averaged over 100 seeds."""
+    S = datagen.random_gaussian_sketch(20, 500, seed=1)
+    assert torch.equal(S, datagen.random_gaussian_sketch(20, 500, seed=1))
+    se = (1.0 / 20) ** 0.5 / (S.numel() ** 0.5)
+    assert abs(float(S.double().mean())) <= 5 * se
+    x = torch.randn(500, dtype=torch.float64, generator=torch.Generator().manual_seed(0))
+    x /= x.norm()
+    vals = [float((datagen.random_gaussian_sketch(20, 500, seed=s).double() @ x).pow(2).sum()) for s in range(100)]
+    assert abs(sum(vals) / len(vals) - 1.0) <= 0.2
