@@ -74,6 +74,9 @@ typedef struct {
   int dense_max_m;   /* m <= this: one dense Jacobi eigensolve of G; default 256 */
   int gemm_chain;    /* tuning: K-chunks per TMEM accumulation chain (0 = default) */
   int gemm_splits;   /* tuning: K splits of the Gram (0 = auto) */
+  const float* init_S; /* optional DEVICE [k][m] warm start of the subspace iteration (e.g. the sketch of
+                          the stream so far); NULL = deterministic pseudo-random start.
+                          Only the starting block changes: S is still the top-k of G to tol. */
 } tsk_train_opts;
 
 typedef struct {

@@ -43,7 +43,8 @@ class TskError(RuntimeError):
 
 class TrainOpts(ctypes.Structure):
     _fields_ = [("oversample", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
-                ("dense_max_m", ctypes.c_int), ("gemm_chain", ctypes.c_int), ("gemm_splits", ctypes.c_int)]
+                ("dense_max_m", ctypes.c_int), ("gemm_chain", ctypes.c_int), ("gemm_splits", ctypes.c_int),
+                ("init_S", ctypes.c_void_p)]
 
 
 class TrainInfo(ctypes.Structure):
@@ -199,6 +200,10 @@ def _opts(opts) -> Optional[TrainOpts]:
         return opts
     o = TrainOpts()
     for k, v in dict(opts).items():
+        if isinstance(v, torch.Tensor):  # device array fields (init_S): pass the pointer
+            if not v.is_cuda or v.dtype != torch.float32 or not v.is_contiguous():
+                raise ValueError(f"{k}: expected a contiguous float32 CUDA tensor")
+            v = v.data_ptr()
         setattr(o, k, v)
     return o
 

@@ -131,6 +131,14 @@ __global__ void write_sketch_kernel(const double* __restrict__ V, int m, int ldv
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Y[i][c] = S0[c][i] for c < k (Y: [m][p] fp64, S0: [k][m] fp32)
+__global__ void init_cols_kernel(double* __restrict__ Y, int m, int p, const float* __restrict__ S0, int k) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)m * k) return;
+  const int c = (int)(e / m), i = (int)(e % m);
+  Y[(size_t)i * p + c] = (double)S0[(size_t)c * m + i];
+}
+
 // Y = Z diag(scale)   (m x p, row-major)
 __global__ void colscale_kernel(const double* __restrict__ Z, const double* __restrict__ scale, int m, int p,
                                 double* __restrict__ Y) {
@@ -278,6 +286,10 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
   g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(Gd, m, ms, G32);
   hash_fill_kernel<<<nblk((long long)mp, 256), 256, 0, s>>>(Y, m, p, 0x5EEDull, 1.0, 0);
   ctx->count_launch(2);
+  if (opt.init_S) {  // warm start: the first k columns of the starting block are the given rows
+    init_cols_kernel<<<nblk((long long)m * k, 256), 256, 0, s>>>(Y, m, p, opt.init_S, k);
+    ctx->count_launch();
+  }
   cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
   if ((st = cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags)) != TSK_OK) return st;
 
