@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&mapX);
     tma_prefetch_desc(&mapY);
     for (int i = 0; i < RS; ++i) {
-      mbar_init(&rfull[i], 1);
+      mbar_init(&rfull[i], 2);  // X box + Y box (or the diagonal tile's plain arrive)
       mbar_init(&rempty[i], 1);
     }
     for (int i = 0; i < kTsLoStages; ++i) {
@@ -431,25 +431,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool diag = a.sym && bi == bj;
       const int s_split = u / a.T;
       const int round = u / gridDim.x;
-      for (long long q = q0; q < q1; ++q) {
-        if (lane == 0) {
-          mbar_wait(&rempty[st], ph ^ 1);
-          const uint32_t ybytes = kYT ? (uint32_t)(a.bn * kBK * 4) : (uint32_t)kTileBytes;
-          mbar_arrive_expect_tx(&rfull[st], diag ? (uint32_t)kTileBytes : (uint32_t)kTileBytes + ybytes);
+      // lanes 0-3 issue the X boxes and lanes 4-7 the Y boxes of 4 consecutive chunks (a thread's TMA
+      // boxes complete one after another; scripts/tma_bench.cu); rfull expects both arrivals
+      const uint32_t ybytes = (uint32_t)(a.bn * kBK * 4);
+      for (long long qb = q0; qb < q1; qb += 4) {
+        const int j = lane & 3;
+        const long long q = qb + j;
+        if (lane < 8 && q < q1) {
+          const int sl = (st + j) % RS;
+          const uint32_t pl = ph ^ (uint32_t)(((st + j) / RS) & 1);
+          mbar_wait(&rempty[sl], pl ^ 1);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
-          if (a.xt) tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], bi * kBM, kc, z);  // box {128 M, 32 K}
-          else tma_load_3d(raw_ptr(st, 0), &mapX, &rfull[st], kc, bi * kBM, z);
-          if (!diag) {
-            if (kYT) tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], bj * a.bn, kc, a.ybc ? 0 : z);  // box {bn N, 32 K}
-            else tma_load_3d(raw_ptr(st, 1), &mapY, &rfull[st], kc, bj * a.bn, a.ybc ? 0 : z);
+          if (lane < 4) {
+            mbar_arrive_expect_tx(&rfull[sl], (uint32_t)kTileBytes);
+            if (a.xt) tma_load_3d(raw_ptr(sl, 0), &mapX, &rfull[sl], bi * kBM, kc, z);  // box {128 M, 32 K}
+            else tma_load_3d(raw_ptr(sl, 0), &mapX, &rfull[sl], kc, bi * kBM, z);
+          } else if (diag) {
+            mbar_arrive(&rfull[sl]);  // the diagonal tile's Y is its X
+          } else {
+            mbar_arrive_expect_tx(&rfull[sl], ybytes);
+            if (kYT) tma_load_3d(raw_ptr(sl, 1), &mapY, &rfull[sl], bj * a.bn, kc, a.ybc ? 0 : z);  // {bn N, 32 K}
+            else tma_load_3d(raw_ptr(sl, 1), &mapY, &rfull[sl], kc, bj * a.bn, a.ybc ? 0 : z);   // {32 K, bn N}
           }
         }
-        if (++st == RS) { st = 0; ph ^= 1; }
-        const unsigned done = (unsigned)(q - q0 + 1);
-        if (a.lag > 0 && ((done & 31u) == 0 || q + 1 == q1)) {
-          if (lane == 0) st_volatile_u32(&a.progress[u], q + 1 == q1 ? 0xFFFFFFFFu : done);
-          if (q + 1 < q1) {
+        __syncwarp();
+        const int nq = (int)min(4LL, q1 - qb);
+        ph ^= (uint32_t)(((st + nq) / RS) & 1);
+        st = (st + nq) % RS;
+        const unsigned done = (unsigned)(qb - q0 + nq);
+        if (a.lag > 0 && ((done & 31u) == 0 || qb + nq == q1)) {
+          if (lane == 0) st_volatile_u32(&a.progress[u], qb + nq == q1 ? 0xFFFFFFFFu : done);
+          if (qb + nq < q1) {
             while (true) {
               unsigned mn = 0xFFFFFFFFu;
               for (int tp = lane; tp < a.T; tp += 32) {
@@ -592,8 +605,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           const uint32_t src = smem_u32(raw_ptr(rs, diag ? 0 : 1));
           const uint32_t dst = smem_u32(lo_ptr(ls));
-#pragma unroll
-          for (int i = 0; i < kTileBytes / 16 / 128; ++i) {
+          const int nyv = a.bn * (kBK * 4 / 16);  // float4 of the bn used rows
+          for (int i = 0; i < nyv / 128; ++i) {
             const uint32_t off = (uint32_t)(i * 128 + tt) * 16u;
             const float4 v = lds_f4(src + off);
             float4 l;
@@ -761,12 +774,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 // 3-D map over [slices][rows][inner] fp32, box [1][128][32], 128-byte swizzle, OOB -> 0.
 static bool make_map_3d(CUtensorMap* map, const float* base, int inner, int rows, long long slices,
-                        long long row_stride_elems, long long slice_stride_elems) {
+                        long long row_stride_elems, long long slice_stride_elems, int box_rows = kBM) {
   auto enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)slices};
   cuuint64_t strides[2] = {(cuuint64_t)(row_stride_elems * 4), (cuuint64_t)(slice_stride_elems * 4)};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)kBM, 1};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -836,7 +849,8 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
       if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: transposed Y tensor map rejected\n");
       return TSK_ECUDA;
     }
-  } else if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride)) {
+  } else if (!make_map_3d(&my, p.Y, p.n, p.N, p.D, p.y_row_stride, p.y_slice_stride,
+                          (p.bn == 64 && !p.sym) ? 64 : kBM)) {
     if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gemm: Y tensor map rejected\n");
     return TSK_ECUDA;
   }

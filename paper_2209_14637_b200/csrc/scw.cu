@@ -323,15 +323,28 @@ __global__ void __launch_bounds__(256, 2) scw_residual_tiled2_kernel(const float
                                                                   const float* __restrict__ L,
                                                                   const float* __restrict__ R, int m, int n,
                                                                   int r, double* __restrict__ part) {
-  extern __shared__ __align__(16) float rsm[];  // Lt [r][128], Rt [r][128]
+  extern __shared__ __align__(16) float rsm[];  // Lt [r][128], Rt [r][128], As [128][128]
   float* Lt = rsm;
   float* Rt = rsm + (size_t)r * 128;
+  float* As = rsm + (size_t)2 * r * 128;
   __shared__ double red[8];
   const int b = blockIdx.z;
   const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const float* Lb = L + (size_t)b * m * r;
   const float* Rb = R + (size_t)b * n * r;
+  const float* Ab = A + (size_t)b * m * n;
+  // the A tile streams into shared memory (cp.async, zero-filled outside the matrix) while the
+  // rank-r product is formed; n % 4 == 0 (ABI), so 16-byte pieces never straddle a row end
+  for (int q = tid; q < 128 * 32; q += 256) {
+    const int row = q >> 5, c4 = q & 31;
+    const int gr = i0 + row, gc = j0 + 4 * c4;
+    const bool in = gr < m && gc < n;
+    const float* src = Ab + (in ? (size_t)gr * n + gc : 0);
+    const uint32_t dst = smem_u32(As + row * 128 + 4 * c4);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int e = tid; e < 128 * r; e += 256) {
     const int row = e % 128, c = e / 128;  // conflict-free transposed stores
     Lt[c * 128 + row] = (i0 + row < m) ? Lb[(size_t)(i0 + row) * r + c] : 0.f;
@@ -356,9 +369,9 @@ __global__ void __launch_bounds__(256, 2) scw_residual_tiled2_kernel(const float
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(lv[i], rv[j], acc[i][j]);
   }
-  const float* Ab = A + (size_t)b * m * n;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
   double sacc = 0.0;
-  const bool vec = (n % 4) == 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int row = i0 + ty + 16 * i;
@@ -366,20 +379,13 @@ __global__ void __launch_bounds__(256, 2) scw_residual_tiled2_kernel(const float
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int col = j0 + 64 * h + tx * 4;
-      float av[4];
-      if (vec && col + 3 < n) {
-        const float4 v = *reinterpret_cast<const float4*>(Ab + (size_t)row * n + col);
-        av[0] = v.x; av[1] = v.y; av[2] = v.z; av[3] = v.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) av[q] = (col + q < n) ? Ab[(size_t)row * n + col + q] : 0.f;
-      }
+      if (col >= n) continue;  // n % 4 == 0: a float4 piece is either inside or outside
+      const float4 v = *reinterpret_cast<const float4*>(As + (ty + 16 * i) * 128 + 64 * h + tx * 4);
+      const float av[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (col + q < n) {
-          const double d = (double)av[q] - (double)acc[i][4 * h + q];
-          sacc += d * d;
-        }
+        const double d = (double)av[q] - (double)acc[i][4 * h + q];
+        sacc += d * d;
       }
     }
   }
@@ -404,7 +410,7 @@ static void scw_attrs() {
     cudaFuncSetAttribute(scw_combine_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
-    cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 128 * 4);
+    cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (2 * 64 * 128 + 128 * 128) * 4);
     attr = true;
   }
 }
@@ -519,7 +525,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     // 6. dense residual
     if (err) {
       dim3 gres(nb(n, 128), nb(m, 128), bc);
-      scw_residual_tiled2_kernel<<<gres, 256, (size_t)2 * r * 128 * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
+      scw_residual_tiled2_kernel<<<gres, 256, ((size_t)2 * r * 128 + 128 * 128) * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
       if ((st = launch_status("scw residual")) != TSK_OK) return st;
       scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
       ctx->count_launch(2);
@@ -643,7 +649,7 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     // 6. dense residual
     if (err) {
       dim3 gres(nb(n, 128), nb(m, 128), bc);
-      scw_residual_tiled2_kernel<<<gres, 256, (size_t)2 * r * 128 * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
+      scw_residual_tiled2_kernel<<<gres, 256, ((size_t)2 * r * 128 + 128 * 128) * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
       scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
       ctx->count_launch(2);
     }
