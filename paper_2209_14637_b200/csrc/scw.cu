@@ -22,63 +22,64 @@
 
 namespace tsk {
 
-// ---------------------------------------------------------------- 2. V^T = diag(mu^-1/2) W^T B
-// thread per column j: its B column (k values) is cached in registers, W comes from shared memory
-template <int KMAX>
-__global__ void __launch_bounds__(128) scw_vt_kernel(const float* __restrict__ Bm, const double* __restrict__ Wc,
-                                                     const double* __restrict__ mu, int k, int n,
-                                                     float* __restrict__ Vt) {
-  extern __shared__ double ws[];  // [k][k] W, then [k] scale
+// ---------------------------------------------------------------- fp64-coefficient combinations
+// Out_b[c][j] (kVt) or Out_b[j][c] = sc_c sum_{a<k} W_b[a][c] In_b[a][j],  c < nout, j < len
+// (kVt: V^T = L^{-1} P B with sc from mu; else the factors L = Z W_r, R = V W_r with sc = 1).
+// Thread per column j: its k inputs are read once into registers (fp32), each is converted to fp64
+// once per 16-wide block of outputs, and the 16 fp64 accumulators take the coefficients from shared
+// memory as broadcast reads.
+template <int KMAX, bool kVt>
+__global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
+                                                          const double* __restrict__ mu, int k, int len, int nout,
+                                                          int ldw, long long wst, float* __restrict__ Out) {
+  extern __shared__ double wsm[];  // [k][nout] coefficients, then [nout] scales
   const int b = blockIdx.y;
-  const double* Wb = Wc + (size_t)b * k * k;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) ws[e] = Wb[e];
-  double* sc = ws + k * k;
-  for (int c = threadIdx.x; c < k; c += blockDim.x) {
-    const double m0 = mu[(size_t)b * k];
-    const double mc = mu[(size_t)b * k + c];
-    sc[c] = (mc > 0.0 && mc > 1e-13 * m0) ? 1.0 / sqrt(mc) : 0.0;
+  const double* Wb = W + (size_t)b * wst;
+  for (int e = threadIdx.x; e < k * nout; e += blockDim.x) wsm[e] = Wb[(size_t)(e / nout) * ldw + (e % nout)];
+  double* sc = wsm + (size_t)k * nout;
+  for (int c = threadIdx.x; c < nout; c += blockDim.x) {
+    if (kVt) {
+      const double m0 = mu[(size_t)b * k];
+      const double mc = mu[(size_t)b * k + c];
+      sc[c] = (mc > 0.0 && mc > 1e-13 * m0) ? 1.0 / sqrt(mc) : 0.0;
+    } else {
+      sc[c] = 1.0;
+    }
   }
   __syncthreads();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const float* Bb = Bm + (size_t)b * k * n;
-  float bv[KMAX];
-#pragma unroll
-  for (int a = 0; a < KMAX; ++a) bv[a] = a < k ? Bb[(size_t)a * n + j] : 0.f;
-  float* Vb = Vt + (size_t)b * k * n;
-  for (int c = 0; c < k; ++c) {
-    double s = 0.0;
-#pragma unroll
-    for (int a = 0; a < KMAX; ++a)
-      if (a < k) s += ws[a * k + c] * (double)bv[a];
-    Vb[(size_t)c * n + j] = (float)(s * sc[c]);
-  }
-}
-
-// ---------------------------------------------------------------- 5. out[i][c] = sum_a In[a][i] W[a][c], c < r
-// coefficient matrix of matrix b: W + b * wst, row stride ldw (W[a][c] at a * ldw + c)
-template <int KMAX>
-__global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
-                                                          int k, int len, int r, int ldw, long long wst,
-                                                          float* __restrict__ Out) {
-  extern __shared__ double wsm[];  // [k][r]
-  const int b = blockIdx.y;
-  const double* Wb = W + (size_t)b * wst;
-  for (int e = threadIdx.x; e < k * r; e += blockDim.x) wsm[e] = Wb[(size_t)(e / r) * ldw + (e % r)];
-  __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= len) return;
+  if (j >= len) return;
   const float* Ib = In + (size_t)b * k * len;
-  float iv[KMAX];
+  constexpr bool kReg = false;  // inputs re-read through L1 per output block (registers for occupancy)
+  float iv[kReg ? KMAX : 1];
+  if (kReg) {
 #pragma unroll
-  for (int a = 0; a < KMAX; ++a) iv[a] = a < k ? Ib[(size_t)a * len + i] : 0.f;
-  float* Ob = Out + (size_t)b * len * r;
-  for (int c = 0; c < r; ++c) {
-    double s = 0.0;
+    for (int a = 0; a < (kReg ? KMAX : 1); ++a) iv[a] = a < k ? Ib[(size_t)a * len + j] : 0.f;
+  }
+  float* Ob = Out + (size_t)b * nout * len;
+  for (int c0 = 0; c0 < nout; c0 += 16) {
+    double s[16];
 #pragma unroll
-    for (int a = 0; a < KMAX; ++a)
-      if (a < k) s += (double)iv[a] * wsm[a * r + c];
-    Ob[(size_t)i * r + c] = (float)s;
+    for (int q = 0; q < 16; ++q) s[q] = 0.0;
+#pragma unroll(kReg ? KMAX : 4)
+    for (int a = 0; a < KMAX; ++a) {
+      if (a < k) {
+        const double x = kReg ? (double)iv[kReg ? a : 0] : (double)Ib[(size_t)a * len + j];
+        const double* wr = wsm + (size_t)a * nout + c0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (c0 + q < nout) s[q] = fma(wr[q], x, s[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int c = c0 + q;
+      if (c < nout) {
+        const float v = (float)(s[q] * sc[c]);
+        if (kVt) Ob[(size_t)c * len + j] = v;
+        else Ob[(size_t)j * nout + c] = v;
+      }
+    }
   }
 }
 
@@ -405,10 +406,10 @@ static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / 
 static void scw_attrs() {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(scw_vt_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_vt_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_combine_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(scw_combine_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(scw_combine_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
     cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (2 * 64 * 128 + 128 * 128) * 4);
     attr = true;
@@ -477,8 +478,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) {
       return st;
     }
-    if (k <= 64) scw_vt_kernel<64><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
-    else scw_vt_kernel<128><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, Vt);
+    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt);
+    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt);
     if ((st = launch_status("scw vt")) != TSK_OK) return st;
     // 3. Z^T = V^T A^T
     {
@@ -511,11 +512,11 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
     if (k <= 64) {
-      scw_combine_kernel<64><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, k, (long long)kk, Lc);
-      scw_combine_kernel<64><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k, (long long)kk, Rc);
+      scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc);
+      scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc);
     } else {
-      scw_combine_kernel<128><<<dim3(nb(m, 128), bc), 128, (size_t)k * r * 8, s>>>(Zt, W2, k, m, r, k, (long long)kk, Lc);
-      scw_combine_kernel<128><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k, (long long)kk, Rc);
+      scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc);
+      scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc);
     }
     ctx->count_launch(2);
     if (sigma) {
@@ -590,8 +591,8 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     }
     launch_gram_rows_tiled(Bm, k, n, bc, Cq, s);
     chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cq, k, Wq, muq);
-    if (k <= 64) scw_vt_kernel<64><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, Vt);
-    else scw_vt_kernel<128><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, Vt);
+    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt);
+    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt);
     ctx->count_launch(3);
     if ((st = launch_status("scw2 Q")) != TSK_OK) return st;
     // 2. P^T: W A_b^T = (A_b W^T)^T (tcgen05, W broadcast, transposed store), same orthonormalisation
@@ -606,8 +607,8 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     }
     launch_gram_rows_tiled(Yt, l, m, bc, Cp, s);
     chol_basis_kernel<<<bc, 128, (size_t)2 * l * (l + 1) * 8, s>>>(Cp, l, Wp, mup);
-    if (l <= 64) scw_vt_kernel<64><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, Pt);
-    else scw_vt_kernel<128><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, Pt);
+    if (l <= 64) scw_combine_kernel<64, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt);
+    else scw_combine_kernel<128, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt);
     ctx->count_launch(3);
     if ((st = launch_status("scw2 P")) != TSK_OK) return st;
     // 3. A_b Q as Z^T = Q^T A_b^T (tcgen05), then M = P^T (A_b Q) as an fp64 cross Gram of rows
@@ -631,14 +632,14 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
     if (k <= 64 && l <= 64) {
-      scw_combine_kernel<64><<<dim3(nb(m, 128), bc), 128, (size_t)l * r * 8, s>>>(Pt, CL, l, m, r, r,
+      scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)l * r + r) * 8, s>>>(Pt, CL, nullptr, l, m, r, r,
                                                                                  (long long)l * r, Lc);
-      scw_combine_kernel<64><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k,
+      scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k,
                                                                                  (long long)kk, Rc);
     } else {
-      scw_combine_kernel<128><<<dim3(nb(m, 128), bc), 128, (size_t)l * r * 8, s>>>(Pt, CL, l, m, r, r,
+      scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)l * r + r) * 8, s>>>(Pt, CL, nullptr, l, m, r, r,
                                                                                   (long long)l * r, Lc);
-      scw_combine_kernel<128><<<dim3(nb(n, 128), bc), 128, (size_t)k * r * 8, s>>>(Vt, W2, k, n, r, k,
+      scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k,
                                                                                   (long long)kk, Rc);
     }
     ctx->count_launch(3);
