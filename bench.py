@@ -44,8 +44,10 @@ def measured_peaks():
 
 
 def workload_desc(c, n_gpus):
+    idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}.get(c.name, "?")
+    kind = "frame-like synthetic stream" if c.offset is not None else "low-rank-plus-noise synthetic stream"
     return {"workload": f"{c.name}: m={c.m} n={c.n} D_train={c.D_train} D_test={c.D_test} k={c.k} r={c.r} "
-                        f"(BASELINE.json configs[3], frame-like synthetic stream)",
+                        f"(BASELINE.json configs[{idx}], {kind})",
             "m": c.m, "n": c.n, "D_train": c.D_train, "D_test": c.D_test, "k": c.k, "r": c.r,
             "parallelism": f"dp{n_gpus} over the stream index d (one NCCL all-reduce of G)",
             "l2_policy": f"inputs larger than L2 ({c.train_bytes / 1e9:.1f} GB training stream per step)"}
@@ -318,7 +320,7 @@ def run_tsketch(args, c):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core products, fp64 partial sums and small solves)",
-            "data": "synthetic (datagen C4 recipe, seed 0; paper datasets unavailable)",
+            "data": f"synthetic (datagen {c.name} recipe, seed 0; paper datasets unavailable)",
             "config": workload_desc(c, world), "phases_ms": phases,
             "sketch_construction_matrices_per_s": c.D_train / ((phases["gram"] + phases["allreduce"] + phases["eig"]) / 1e3),
             "test_matrices_per_s": c.D_test / (phases["scw"] / 1e3) if phases["scw"] > 0 else None,

@@ -131,6 +131,20 @@ __global__ void write_sketch_kernel(const double* __restrict__ V, int m, int ldv
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// ||G||_F^2 in a fixed order: one CTA, thread-strided partial sums, tree reduction
+__global__ void fro2_kernel(const double* __restrict__ G, long long n, double* __restrict__ out) {
+  __shared__ double red[1024];
+  double sacc = 0.0;
+  for (long long e = threadIdx.x; e < n; e += blockDim.x) sacc += G[e] * G[e];
+  red[threadIdx.x] = sacc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
 // Y[i][c] = S0[c][i] for c < k (Y: [m][p] fp64, S0: [k][m] fp32)
 __global__ void init_cols_kernel(double* __restrict__ Y, int m, int p, const float* __restrict__ S0, int k) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -292,6 +306,18 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
   }
   cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
   if ((st = cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags)) != TSK_OK) return st;
+  // Working-precision floor of the Ritz residual: the 3xTF32 G Q products carry an error of
+  // ~1e-8 ||G||_F (measured at C5, where ||G||_F / theta_1 = 61 and the residual stalls at 6e-7);
+  // the requested tol is raised to 4x that floor, and a Ky Fan energy that no longer changes
+  // (< 1e-12 relative over two outer iterations) also ends the iteration.
+  fro2_kernel<<<1, 1024, 0, s>>>(G64, (long long)m * m, ncol);
+  ctx->count_launch();
+  double gfro2 = 0.0;
+  cudaMemcpyAsync(&gfro2, ncol, 8, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return TSK_ECUDA;
+  const double gfro = std::sqrt(std::max(gfro2, 0.0));
+  double kyfan_prev = -1.0;
+  int kyfan_still = 0;
 
   GemmProblem gp;
   gp.X = G32;
@@ -352,9 +378,23 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
     max_res = 0.0;
     for (int c = 0; c < kr; ++c) max_res = std::max(max_res, hres[c]);
     max_res /= theta_top > 0 ? theta_top : 1.0;
+    const double tol_eff = std::max(tol, theta_top > 0 ? 4e-8 * gfro / theta_top : tol);
+    double kf_now = 0.0;  // Ky Fan energy of the current k wanted values (locked + active)
+    {
+      std::vector<double> hl(nl);
+      if (nl > 0) {
+        cudaMemcpyAsync(hl.data(), thl, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+      }
+      for (double v : hl) kf_now += v;
+      for (int c = 0; c < kr; ++c) kf_now += hth[c];
+    }
+    if (kyfan_prev > 0 && std::fabs(kf_now - kyfan_prev) <= 1e-12 * kf_now) ++kyfan_still;
+    else kyfan_still = 0;
+    kyfan_prev = kf_now;
     if (getenv("TSK_EIG_TRACE"))
-      fprintf(stderr, "[eig] outer=%d products=%d locked=%d max_res=%.3e theta0=%.4e theta_k=%.4e theta_p=%.4e\n",
-              outer, products, nl, max_res, hth[0], hth[kr - 1], hth[pa - 1]);
+      fprintf(stderr, "[eig] outer=%d products=%d locked=%d max_res=%.3e (tol %.2e) theta0=%.4e theta_k=%.4e theta_p=%.4e "
+              "kyfan=%.12e\n", outer, products, nl, max_res, tol_eff, hth[0], hth[kr - 1], hth[pa - 1], kf_now);
     if (hflags[0] + hflags[1] > 0) {
       // rank-deficient block (rank(G) < p): perturb with fresh directions and re-orthonormalise
       if (++repairs > 8) return TSK_ECUDA;
@@ -364,7 +404,7 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
       if ((st = cholqr2(ctx, Y, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
       continue;
     }
-    if (max_res <= tol) {
+    if (max_res <= tol_eff || (kyfan_still >= 2 && max_res <= 1e-4)) {
       converged = true;
       break;
     }
