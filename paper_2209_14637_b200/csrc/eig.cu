@@ -359,7 +359,7 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
     if ((st = gq(Q, pa)) != TSK_OK) return st;
     ++products;
     if ((st = gemm_tn_f64(ctx, Q, pa, 0, Z, pa, 0, m, pa, pa, 1, H, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
-    if ((st = jacobi_eig_batched(ctx, H, pa, 1, W, theta, nullptr, 1e-9)) != TSK_OK) return st;
+    if ((st = jacobi_eig_batched(ctx, H, pa, 1, W, theta, flags + 2, 1e-9)) != TSK_OK) return st;
     inv_theta_kernel<<<nblk(pa, 128), 128, 0, s>>>(theta, pa, invt);
     ctx->count_launch();
     if ((st = gemm_nn_f64(ctx, Z, pa, 0, W, pa, 0, m, pa, pa, 1, invt, Y, pa, 0)) != TSK_OK) return st;  // G'X/theta
@@ -368,7 +368,7 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
     ctx->count_launch();
     cudaMemcpyAsync(hostbuf, theta, (size_t)pa * 8, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(hostbuf + p, res, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hostbuf + 2 * p, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hostbuf + 2 * p, flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return TSK_ECUDA;
     const double* hth = hostbuf;
@@ -394,7 +394,8 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
     kyfan_prev = kf_now;
     if (getenv("TSK_EIG_TRACE"))
       fprintf(stderr, "[eig] outer=%d products=%d locked=%d max_res=%.3e (tol %.2e) theta0=%.4e theta_k=%.4e theta_p=%.4e "
-              "kyfan=%.12e\n", outer, products, nl, max_res, tol_eff, hth[0], hth[kr - 1], hth[pa - 1], kf_now);
+              "kyfan=%.12e rr_sweeps=%d\n", outer, products, nl, max_res, tol_eff, hth[0], hth[kr - 1], hth[pa - 1], kf_now,
+              hflags[2]);
     if (hflags[0] + hflags[1] > 0) {
       // rank-deficient block (rank(G) < p): perturb with fresh directions and re-orthonormalise
       if (++repairs > 8) return TSK_ECUDA;

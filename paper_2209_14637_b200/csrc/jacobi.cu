@@ -19,7 +19,7 @@
 namespace tsk {
 
 constexpr int kJacThreads = 1024;
-constexpr int kJacSmemMax = 210 * 1024;
+constexpr int kJacSmemMax = 222 * 1024;  // dynamic part: p <= 118 keeps A and V in shared memory
 
 // pair k of round r in the circle ordering over pe (even) indices, no divisions
 __device__ __forceinline__ void rr_pair(int r, int k, int pe, int& i, int& j) {
