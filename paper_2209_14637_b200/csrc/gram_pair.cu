@@ -49,11 +49,13 @@ constexpr int kStageBytes = kXBytes + kYBytes;  // 48 KB (multiple of 1024: SW12
 constexpr int kRaw = 4;                  // TMA ring (stages of kZ chunks)
 constexpr int kLo = 4;                   // transform ring, per CHUNK (L_Y in smem + [H_X | L_X] in TMEM)
 constexpr int kThreads = 512;
-constexpr int kAccCols = 128;            // one accumulator buffer (two buffers)
+constexpr int kAccCols = 128;            // one accumulator buffer
+constexpr int kAccBufs = 2;              // accumulator buffers (double-buffered: drains overlap the MMA;
+                                         // 1 buffer + 6 A stages measured no faster)
 constexpr int kAStageCols = 64;          // per chunk: H_X 32 cols + L_X 32 cols
-constexpr int kTmemCols = 512;           // 2 * 128 + 4 * 64
+constexpr int kTmemCols = 512;           // kAccBufs * 128 + kLo * 64
 constexpr int kSmemBytes = kRaw * kStageBytes + kLo * kYSub + 1024 + 256;
-static_assert(2 * kAccCols + kLo * kAStageCols <= kTmemCols, "TMEM budget");
+static_assert(kAccBufs * kAccCols + kLo * kAStageCols <= kTmemCols, "TMEM budget");
 static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 struct PairUnit {
@@ -119,7 +121,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&lfull[i], 12);  // 6 transform warps x 2 CTAs
       mbar_init(&lempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(&accf[i], 1);
       mbar_init(&acce[i], 16);   // 8 epilogue warps x 2 CTAs
     }
@@ -151,10 +153,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int yrow0 = pu.J * kBM + (int)crank * yrows;
       const CUtensorMap* my = pu.nb == 128 ? &mapY64 : &mapY32;
       const int round = u / nclusters;
-      for (long long qb = pu.q0; qb < pu.q1; qb += 4) {
-        const int j = lane & 3;
+      // group of kGrp consecutive stages per pass: never two lanes on the same stage (a lane waiting
+      // for a phase that another lane of its own warp must produce could stall the warp)
+      constexpr int kGrp = kRaw < 4 ? kRaw : 4;
+      for (long long qb = pu.q0; qb < pu.q1; qb += kGrp) {
+        const int j = lane % kGrp;
         const long long q = qb + j;
-        if (lane < 8 && q < pu.q1) {
+        if (lane < 2 * kGrp && q < pu.q1) {
           const int sl = (st + j) % kRaw;
           const uint32_t pl = ph ^ (uint32_t)(((st + j) / kRaw) & 1);
           (kSpin ? mbar_wait_spin : mbar_wait)(&rempty[sl], pl ^ 1);
@@ -162,7 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int kc = (int)(q % a.cps) * kBK;
           if (a.diag & 4) {  // diagnostics: no loads (operands are whatever the ring holds)
             mbar_arrive(&rfull[sl]);
-          } else if (lane < 4) {
+          } else if (lane < kGrp) {
             mbar_arrive_expect_tx(&rfull[sl], (uint32_t)kXBytes);
             tma_load_3d(x_ptr(sl), &mapX, &rfull[sl], kc, xi * kBM, z);
           } else {
@@ -171,7 +176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
-        const int nq = (int)min(4LL, pu.q1 - qb);
+        const int nq = (int)min((long long)kGrp, pu.q1 - qb);
         tq += nq;
         ph ^= (uint32_t)(((st + nq) / kRaw) & 1);
         st = (st + nq) % kRaw;
@@ -231,7 +236,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             tstamp(a, cid, 1, ti);
             const uint32_t d = tmem_base + (uint32_t)ab * kAccCols;
-            const uint32_t a_hi = tmem_base + 2 * kAccCols + (uint32_t)ls * kAStageCols;
+            const uint32_t a_hi = tmem_base + kAccBufs * kAccCols + (uint32_t)ls * kAStageCols;
             const uint32_t a_lo = a_hi + 32;
             const uint64_t yh = sw128_kmajor_desc(smem_u32(y_ptr(rs)) + zs * ysub);
             const uint64_t yl = sw128_kmajor_desc(smem_u32(l_ptr(ls)));
@@ -251,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (++cpos == a.chain || (q + 1 == pu.q1 && zs + 1 == kZ)) {
               mma2_commit_mc(&accf[ab], 3);
               cpos = 0;
-              if (++ab == 2) { ab = 0; aph ^= 1; }
+              if (++ab == kAccBufs) { ab = 0; aph ^= 1; }
             }
           }
           mma2_commit_mc(&rempty[rs], 3);
@@ -300,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
               }
               const uint32_t ta =
-                  tmem_base + ((uint32_t)(quad * 32) << 16) + 2 * kAccCols + (uint32_t)ls * kAStageCols;
+                  tmem_base + ((uint32_t)(quad * 32) << 16) + kAccBufs * kAccCols + (uint32_t)ls * kAStageCols;
               tmem_st_32x32b_x32(ta, hi);
               tmem_st_32x32b_x32(ta + 32, lo);
             }
@@ -377,7 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (e == 0 && lane == 0 && crank == 0) tstamp(a, cid, 10, tc * 8);
         ++tc;
         if (lane == 0) mbar_arrive_cluster(acce_leader + (uint32_t)ab * 8u);
-        if (++ab == 2) { ab = 0; aph ^= 1; }
+        if (++ab == kAccBufs) { ab = 0; aph ^= 1; }
         if (++cin == a.fold || c + 1 == nchains) {
           const uint64_t pol = l2_policy_evict_last();
           if (first_fold) {
