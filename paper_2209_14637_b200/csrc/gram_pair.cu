@@ -453,7 +453,7 @@ __global__ void gram_pair_finalize_kernel(const double* __restrict__ part, const
 }
 
 // ------------------------------------------------------------------------------ host schedule
-struct Sched {
+struct Sched : HostCache {
   int m = -1, nsm = -1;
   long long Kc = -1;
   int splits_req = -1;
@@ -639,7 +639,9 @@ tsk_status gram_pair(Ctx* ctx, const GemmProblem& p) {
   int ncl = max_clusters;
   if (const char* ev = getenv("TSK_PAIR_CLUSTERS")) ncl = std::max(1, std::min(ncl, atoi(ev)));
 
-  static Sched sched;  // host schedule cache (depends on m, K chunks, clusters, requested splits)
+  // host schedule cache, per ctx (depends on m, K chunks, clusters, requested splits)
+  if (!ctx->gram_sched) ctx->gram_sched.reset(new Sched());
+  Sched& sched = *static_cast<Sched*>(ctx->gram_sched.get());
   const int min_chunks = std::max(1, (p.min_chunks_per_unit > 0 ? p.min_chunks_per_unit : 8) / kZ);
   if (sched.m != m || sched.Kc != Kc || sched.nsm != 2 * ncl || sched.splits_req != p.splits) {
     build_sched(sched, m, Kc, 2 * ncl, p.splits, min_chunks);

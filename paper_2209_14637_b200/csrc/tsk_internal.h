@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 
@@ -52,6 +53,11 @@ enum WorkspaceId {
   WS_COUNT
 };
 
+// per-context host-side caches (e.g. the pair-Gram schedule): owned by the ctx, freed with it
+struct HostCache {
+  virtual ~HostCache() = default;
+};
+
 struct Ctx {
   int device = 0;
   int num_sms = 148;
@@ -97,6 +103,7 @@ struct Ctx {
   // pair-Gram schedule last uploaded to ws[WS_GRAM_SCHED] (pointer + host schedule version)
   const void* gram_sched_dev = nullptr;
   long long gram_sched_ver = -1;
+  std::unique_ptr<HostCache> gram_sched;  // host schedule of the last pair-Gram shape (gram_pair.cu)
 };
 
 struct GemmInfo {
