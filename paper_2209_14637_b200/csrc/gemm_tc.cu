@@ -63,6 +63,10 @@ struct GemmArgs {
   int xt;        // X operand stored transposed ([z][K][M], M contiguous): the transform reads tile columns
   int ybc;       // Y broadcast: every slice z uses Y slice 0
   int drow;      // direct output row-major: dout[b * dstride + row * ldd + col]
+  const float* resA;  // residual epilogue: tile partials of sum (resA_b[row][col] - D[row][col])^2 (fp64)
+  long long res_stride;
+  int res_ld;
+  double* res_part;   // [units][8] (one partial per epilogue warp, fixed order)
   long long dstride;
   int ldd;
 };
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&acce[ab]);
         if (++ab == 2) { ab = 0; aph ^= 1; }
-        if (a.dout) continue;  // direct output: keep summing in fp32, store once at the end
+        if (a.dout || a.resA) continue;  // direct output / residual: keep summing in fp32, use once at the end
         if (++cin == a.fold || c + 1 == nchains) {
           const uint64_t pol = l2_policy_evict_last();
           if (first_fold) {
@@ -698,6 +702,55 @@ __global__ void __launch_bounds__(kThreads, 1)
           first_fold = false;
           cin = 0;
         }
+      }
+      if (a.resA) {
+        // residual epilogue (SCW error): this thread's row segment of A_b minus the
+        // rank-r product D = L R^T of the tile, squared and summed in fp64, warp-reduced
+        int bi, bj;
+        tile_coords(a, t, bi, bj);
+        const int b = t / a.T0;
+        const int gr = bi * kBM + row;
+        double acc = 0.0;
+        if (has_cols && gr < a.Mv) {
+          const float* ar = a.resA + (size_t)b * a.res_stride + (size_t)gr * a.res_ld + (size_t)bj * a.bn + col0;
+          const int nv = min(64, min(a.bn - col0, a.Nv - (bj * a.bn + col0)));
+          if (nv == 64 && ((reinterpret_cast<uintptr_t>(ar) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 64; i += 4) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(ar + i));
+              const double d0 = (double)v.x - (double)sum[i], d1 = (double)v.y - (double)sum[i + 1];
+              const double d2 = (double)v.z - (double)sum[i + 2], d3 = (double)v.w - (double)sum[i + 3];
+              acc += d0 * d0 + d1 * d1 + d2 * d2 + d3 * d3;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+              if (i < nv) {
+                const double d = (double)__ldg(ar + i) - (double)sum[i];
+                acc += d * d;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.res_part[(size_t)u * 8 + e] = acc;
+        // pull this thread's A segment of the CTA's next unit into L2 while its MMAs run
+        const int un = u + (int)gridDim.x;
+        if (un < a.U && has_cols) {
+          int tn, bin, bjn;
+          long long qa, qb;
+          unit_range(a, un, tn, qa, qb);
+          tile_coords(a, tn, bin, bjn);
+          const int grn = bin * kBM + row;
+          const int gcn = bjn * a.bn + col0;
+          if (grn < a.Mv && gcn < a.Nv) {
+            const float* an = a.resA + (size_t)(tn / a.T0) * a.res_stride + (size_t)grn * a.res_ld + gcn;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(an));
+            if (gcn + 32 < a.Nv) asm volatile("prefetch.global.L2 [%0];" ::"l"(an + 32));
+          }
+        }
+        continue;
       }
       if (a.dout && has_cols) {
         // transposed store: for a fixed column, the 32 lanes (consecutive rows) write contiguously
@@ -806,7 +859,7 @@ static int choose_splits(int T, long long Kc, int sms, int min_chunks) {
 
 tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   if (p.M <= 0 || p.N <= 0 || p.n <= 0 || p.D <= 0) return TSK_EINVAL;
-  if ((p.n % 4) || (p.x_row_stride % 4) || (p.y_row_stride % 4) || (p.x_slice_stride % 4) ||
+  if ((p.x_row_stride % 4) || (p.y_row_stride % 4) || (p.x_slice_stride % 4) ||
       (p.y_slice_stride % 4) || (reinterpret_cast<uintptr_t>(p.X) & 15) || (reinterpret_cast<uintptr_t>(p.Y) & 15))
     return TSK_ESHAPE;
   if (p.sym && (p.X != p.Y || p.M != p.N)) return TSK_EINVAL;
@@ -864,7 +917,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.cps = (p.n + kBK - 1) / kBK;
   if (p.batch) {
     // D independent problems; one unit per (problem, tile), results stored directly (fp32)
-    if (p.sym || !p.dout) return TSK_EINVAL;
+    if (p.sym || (!p.dout && !p.resA)) return TSK_EINVAL;
     a.batch = 1;
     a.T0 = mb * nb;
     a.T = (int)(p.D * a.T0);
@@ -881,6 +934,10 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.xt = p.xt;
   a.ybc = p.ybc;
   a.drow = p.drow;
+  a.resA = p.resA;
+  a.res_stride = p.res_stride;
+  a.res_ld = p.res_ld;
+  a.res_part = p.res_part;
   a.dout = p.dout;
   a.dstride = p.dstride;
   a.ldd = p.ldd;
@@ -890,7 +947,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.products = p.products == 1 ? 1 : 3;
   a.raw = p.raw;
   a.lag = a.batch ? 0 : (p.lag >= 0 ? p.lag : 64);
-  const size_t part_bytes = a.dout ? 256 : (size_t)a.U * kBM * kBN * sizeof(double);
+  const size_t part_bytes = (a.dout || a.resA) ? 256 : (size_t)a.U * kBM * kBN * sizeof(double);
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_GEMM_PARTIAL, part_bytes));
   if (!part) return TSK_ENOMEM;
   a.part = part;
@@ -934,7 +991,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   }
   if (launch_status("gemm_tf32x3") != TSK_OK) return TSK_ECUDA;
   ctx->count_launch();
-  if (a.dout) {
+  if (a.dout || a.resA) {
     if (p.info) {
       p.info->splits = a.S;
       p.info->units = a.U;

@@ -31,7 +31,7 @@ namespace tsk {
 template <int KMAX, bool kVt>
 __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
                                                           const double* __restrict__ mu, int k, int len, int nout,
-                                                          int ldw, long long wst, float* __restrict__ Out) {
+                                                          int ldw, long long wst, float* __restrict__ Out, int ldo) {
   extern __shared__ double wsm[];  // [k][nout] coefficients, then [nout] scales
   const int b = blockIdx.y;
   const double* Wb = W + (size_t)b * wst;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restric
 #pragma unroll
     for (int a = 0; a < (kReg ? KMAX : 1); ++a) iv[a] = a < k ? Ib[(size_t)a * len + j] : 0.f;
   }
-  float* Ob = Out + (size_t)b * nout * len;
+  float* Ob = Out + (size_t)b * (kVt ? (size_t)nout * len : (size_t)len * ldo);
   for (int c0 = 0; c0 < nout; c0 += 16) {
     double s[16];
 #pragma unroll
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restric
       if (c < nout) {
         const float v = (float)(s[q] * sc[c]);
         if (kVt) Ob[(size_t)c * len + j] = v;
-        else Ob[(size_t)j * nout + c] = v;
+        else Ob[(size_t)j * ldo + c] = v;
       }
     }
   }
@@ -316,92 +316,38 @@ __global__ void __launch_bounds__(128) chol_basis_kernel(const double* __restric
   for (int c = tid; c < k; c += nt) mu[(size_t)b * k + c] = c < rk ? 1.0 : 0.0;
 }
 
-// partial[b][tile] = sum over a [128 x 128] tile of (A - L R^T)^2 ; L [m][r], R [n][r]
-// 256 threads = 16 x 16, each an 8 x 8 block (rows ty + 16 i, cols 4 tx + 64 h + {0..3}): L and R
-// are staged transposed in shared memory, so every contraction step is 2 + 2 float4 loads for 64
-// FMAs; the A tile is read once, coalesced (float4), and (a - s)^2 is summed in fp64.
-__global__ void __launch_bounds__(256, 2) scw_residual_tiled2_kernel(const float* __restrict__ A,
-                                                                  const float* __restrict__ L,
-                                                                  const float* __restrict__ R, int m, int n,
-                                                                  int r, double* __restrict__ part) {
-  extern __shared__ __align__(16) float rsm[];  // Lt [r][128], Rt [r][128], As [128][128]
-  float* Lt = rsm;
-  float* Rt = rsm + (size_t)r * 128;
-  float* As = rsm + (size_t)2 * r * 128;
-  __shared__ double red[8];
-  const int b = blockIdx.z;
-  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const float* Lb = L + (size_t)b * m * r;
-  const float* Rb = R + (size_t)b * n * r;
-  const float* Ab = A + (size_t)b * m * n;
-  // the A tile streams into shared memory (cp.async, zero-filled outside the matrix) while the
-  // rank-r product is formed; n % 4 == 0 (ABI), so 16-byte pieces never straddle a row end
-  for (int q = tid; q < 128 * 32; q += 256) {
-    const int row = q >> 5, c4 = q & 31;
-    const int gr = i0 + row, gc = j0 + 4 * c4;
-    const bool in = gr < m && gc < n;
-    const float* src = Ab + (in ? (size_t)gr * n + gc : 0);
-    const uint32_t dst = smem_u32(As + row * 128 + 4 * c4);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int e = tid; e < 128 * r; e += 256) {
-    const int row = e % 128, c = e / 128;  // conflict-free transposed stores
-    Lt[c * 128 + row] = (i0 + row < m) ? Lb[(size_t)(i0 + row) * r + c] : 0.f;
-    Rt[c * 128 + row] = (j0 + row < n) ? Rb[(size_t)(j0 + row) * r + c] : 0.f;
-  }
-  __syncthreads();
-  float acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
-  for (int c = 0; c < r; ++c) {
-    float lv[8], rv[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) lv[i] = Lt[c * 128 + ty + 16 * i];
-    const float4 r0 = *reinterpret_cast<const float4*>(&Rt[c * 128 + tx * 4]);
-    const float4 r1 = *reinterpret_cast<const float4*>(&Rt[c * 128 + 64 + tx * 4]);
-    rv[0] = r0.x; rv[1] = r0.y; rv[2] = r0.z; rv[3] = r0.w;
-    rv[4] = r1.x; rv[5] = r1.y; rv[6] = r1.z; rv[7] = r1.w;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(lv[i], rv[j], acc[i][j]);
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  double sacc = 0.0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = i0 + ty + 16 * i;
-    if (row >= m) continue;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int col = j0 + 64 * h + tx * 4;
-      if (col >= n) continue;  // n % 4 == 0: a float4 piece is either inside or outside
-      const float4 v = *reinterpret_cast<const float4*>(As + (ty + 16 * i) * 128 + 64 * h + tx * 4);
-      const float av[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double d = (double)av[q] - (double)acc[i][4 * h + q];
-        sacc += d * d;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-  if ((tid & 31) == 0) red[tid >> 5] = sacc;
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < 8; ++w) t += red[w];
-    part[(size_t)b * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = t;
-  }
-}
-
 static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+
+// err_b = ||A_b - L_b R_b^T||_F for factors with row pitch ldf (a multiple of 4): L R^T on tcgen05
+// (3xTF32, K = r, one 128 x 128 tile per unit) with the residual epilogue of gemm_tc.cu reading
+// the A tile and reducing (a - s)^2 in fp64; fixed-order reduction of the per-warp partials.
+static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, const float* Lc, const float* Rc,
+                              int r, int ldf, double* part, double* err) {
+  GemmProblem gp;
+  gp.X = Lc;
+  gp.Y = Rc;
+  gp.M = m;
+  gp.N = n;
+  gp.n = r;
+  gp.D = bc;
+  gp.x_row_stride = ldf;
+  gp.x_slice_stride = (long long)m * ldf;
+  gp.y_row_stride = ldf;
+  gp.y_slice_stride = (long long)n * ldf;
+  gp.batch = 1;
+  gp.bn = 128;
+  gp.resA = Ac;
+  gp.res_stride = (long long)m * n;
+  gp.res_ld = n;
+  gp.res_part = part;
+  tsk_status st = gemm_tf32x3(ctx, gp);
+  if (st != TSK_OK) return st;
+  const int per = (int)(nb(m, 128) * nb(n, 128)) * 8;  // partials per matrix
+  scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, ctx->stream>>>(part, per, bc, err);
+  ctx->count_launch();
+  return launch_status("scw residual (tcgen05)");
+}
 
 static void scw_attrs() {
   static bool attr = false;
@@ -411,7 +357,6 @@ static void scw_attrs() {
     cudaFuncSetAttribute(scw_combine_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
-    cudaFuncSetAttribute(scw_residual_tiled2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (2 * 64 * 128 + 128 * 128) * 4);
     attr = true;
   }
 }
@@ -427,8 +372,10 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   float* Vt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
   float* Zt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
   double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW_3, chunk * (4 * kk + 2 * k) * 8));
-  const int tiles = (int)(nb(n, 128) * nb(m, 128));
-  float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * r * 4));
+  const int tiles = (int)(nb(n, 128) * nb(m, 128)) * 8;  // residual partials per matrix
+  // factor row pitch: r for the caller's L / R, r rounded up to 4 (16-byte TMA rows) for the error path
+  const int ldf = (L || R) ? r : (r + 3) & ~3;
+  float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * ldf * 4));
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
   if (!Bm || !Vt || !Zt || !small || !Lw || !part) return TSK_ENOMEM;
   double* Cb = small;
@@ -478,8 +425,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) {
       return st;
     }
-    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt);
-    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt);
+    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
+    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
     if ((st = launch_status("scw vt")) != TSK_OK) return st;
     // 3. Z^T = V^T A^T
     {
@@ -510,27 +457,21 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10)) != TSK_OK) return st;
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
-    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
+    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf;
     if (k <= 64) {
-      scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc);
-      scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc);
+      scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
+      scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
     } else {
-      scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc);
-      scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc);
+      scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
+      scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
     }
     ctx->count_launch(2);
     if (sigma) {
       scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
       ctx->count_launch();
     }
-    // 6. dense residual
-    if (err) {
-      dim3 gres(nb(n, 128), nb(m, 128), bc);
-      scw_residual_tiled2_kernel<<<gres, 256, ((size_t)2 * r * 128 + 128 * 128) * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
-      if ((st = launch_status("scw residual")) != TSK_OK) return st;
-      scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
-      ctx->count_launch(2);
-    }
+    // 6. dense residual (the error path always has pitch-aligned workspace factors)
+    if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part, err + b0)) != TSK_OK) return st;
     if ((st = launch_status("scw")) != TSK_OK) return st;
   }
   return TSK_OK;
@@ -558,8 +499,9 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
   float* Pt = reinterpret_cast<float*>(ctx->workspace(WS_SCW2_1, chunk * lm * 4));
   const size_t nsmall = chunk * (2 * kk + 2 * ll + 2 * (size_t)l * k + (size_t)l * r + kk + 2 * (size_t)k + 2 * (size_t)l);
   double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW2_2, nsmall * 8));
-  const int tiles = (int)(nb(n, 128) * nb(m, 128));
-  float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * r * 4));
+  const int tiles = (int)(nb(n, 128) * nb(m, 128)) * 8;
+  const int ldf = (L || R) ? r : (r + 3) & ~3;
+  float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * ldf * 4));
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
   if (!Bm || !Vt || !Zt || !Yt || !Pt || !small || !Lw || !part) return TSK_ENOMEM;
   double* Cq = small;                      // [k][k]
@@ -591,8 +533,8 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     }
     launch_gram_rows_tiled(Bm, k, n, bc, Cq, s);
     chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cq, k, Wq, muq);
-    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt);
-    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt);
+    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt, 0);
+    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt, 0);
     ctx->count_launch(3);
     if ((st = launch_status("scw2 Q")) != TSK_OK) return st;
     // 2. P^T: W A_b^T = (A_b W^T)^T (tcgen05, W broadcast, transposed store), same orthonormalisation
@@ -607,8 +549,8 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     }
     launch_gram_rows_tiled(Yt, l, m, bc, Cp, s);
     chol_basis_kernel<<<bc, 128, (size_t)2 * l * (l + 1) * 8, s>>>(Cp, l, Wp, mup);
-    if (l <= 64) scw_combine_kernel<64, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt);
-    else scw_combine_kernel<128, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt);
+    if (l <= 64) scw_combine_kernel<64, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt, 0);
+    else scw_combine_kernel<128, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt, 0);
     ctx->count_launch(3);
     if ((st = launch_status("scw2 P")) != TSK_OK) return st;
     // 3. A_b Q as Z^T = Q^T A_b^T (tcgen05), then M = P^T (A_b Q) as an fp64 cross Gram of rows
@@ -630,17 +572,17 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     // 5. factors: L = P (M W2_r), R = Q W2_r
     small_mm_f64_kernel<<<bc, 256, 0, s>>>(Mx, W2, l, k, r, CL);
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
-    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * r;
+    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf;
     if (k <= 64 && l <= 64) {
       scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)l * r + r) * 8, s>>>(Pt, CL, nullptr, l, m, r, r,
-                                                                                 (long long)l * r, Lc);
+                                                                                 (long long)l * r, Lc, ldf);
       scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k,
-                                                                                 (long long)kk, Rc);
+                                                                                 (long long)kk, Rc, ldf);
     } else {
       scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)l * r + r) * 8, s>>>(Pt, CL, nullptr, l, m, r, r,
-                                                                                  (long long)l * r, Lc);
+                                                                                  (long long)l * r, Lc, ldf);
       scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k,
-                                                                                  (long long)kk, Rc);
+                                                                                  (long long)kk, Rc, ldf);
     }
     ctx->count_launch(3);
     if (sigma) {
@@ -648,12 +590,7 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
       ctx->count_launch();
     }
     // 6. dense residual
-    if (err) {
-      dim3 gres(nb(n, 128), nb(m, 128), bc);
-      scw_residual_tiled2_kernel<<<gres, 256, ((size_t)2 * r * 128 + 128 * 128) * 4, s>>>(Ac, Lc, Rc, m, n, r, part);
-      scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, s>>>(part, (int)(gres.x * gres.y), bc, err + b0);
-      ctx->count_launch(2);
-    }
+    if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part, err + b0)) != TSK_OK) return st;
     if ((st = launch_status("scw2")) != TSK_OK) return st;
   }
   return TSK_OK;

@@ -139,6 +139,11 @@ struct GemmProblem {
   int ybc = 0;            // 1: Y broadcast (slice 0 for every z; TS kernel only)
   int yt = 0;             // 1: Y_z stored transposed, [K = n][N] with N contiguous (y_row_stride = K stride)
   int drow = 0;           // direct output row-major: dout[b * dstride + row * ldd + col]
+  // residual epilogue (batch mode): res_part[unit][8] = sum over the tile of (resA - X Y^T)^2
+  const float* resA = nullptr;
+  long long res_stride = 0;
+  int res_ld = 0;
+  double* res_part = nullptr;
   int bn = 128;           // MMA N tile: 128 or 64
   float* dout = nullptr;  // direct fp32 output, transposed: dout[b * dstride + col * ldd + row]
   long long dstride = 0;
