@@ -90,6 +90,11 @@ __device__ __forceinline__ void unit_range(const GemmArgs& a, int u, int& t, lon
   int s = u / a.T;
   // batched: tile t belongs to problem b = t / T0, whose K range is the chunks of slice b only
   const long long base = a.batch ? (long long)(t / a.T0) * a.cps : 0;
+  if (a.S == 1) {  // batched problems: no 64-bit division per unit
+    q0 = base;
+    q1 = base + a.Kc;
+    return;
+  }
   q0 = base + (long long)s * a.Kc / a.S;
   q1 = base + (long long)(s + 1) * a.Kc / a.S;
 }
