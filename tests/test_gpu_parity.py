@@ -279,3 +279,30 @@ def test_theorem1_holds_for_gpu_outputs():
     Sd = S.cpu().double().numpy()
     bound = validators.theorem1_bound(A.numpy(), Sd, c.r)
     assert float(np.sum(err ** 2)) <= bound * (1 + 1e-5)
+
+
+# ------------------------------------------------------------------------------------- sharding on one GPU
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_virtual_shards_match_single_gram(world):
+    """SURVEY.md §4 "virtual shards": the P partial Grams of the contiguous shards (shard_range),
+    computed one after another on this GPU and summed in rank order (what the all-reduce of the
+    multi-GPU path does), equal the one-shot Gram within rounding, and the sketch from the summed G
+    has the same Ky Fan energy (pin P11, shard count)."""
+    from paper_2209_14637_b200.dist import shard_range
+    c = datagen.CONFIGS["C3"]
+    A = datagen.generate(c, "train", 0, 48, device="cuda")
+    G1, _ = tsk.sketch_gram(A)
+    parts = []
+    for rank in range(world):
+        d0, d1 = shard_range(A.shape[0], rank, world)
+        parts.append(tsk.sketch_gram(A[d0:d1].contiguous())[0])
+    Gs = torch.zeros_like(G1)
+    for Gp in parts:   # rank order
+        Gs += Gp
+    assert relF(Gs.cpu().numpy(), G1.cpu().numpy()) <= 1e-6
+    S1, lam1, _, _ = tsk.sketch_topk(G1, c.k)
+    Ss, lams, _, _ = tsk.sketch_topk(Gs, c.k)
+    Go = tucker1.mode1_gram(A.cpu().numpy())
+    e1 = tucker1.kyfan_energy(Go, S1.cpu().double().numpy())
+    es = tucker1.kyfan_energy(Go, Ss.cpu().double().numpy())
+    assert abs(e1 - es) <= 1e-7 * e1
