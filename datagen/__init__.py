@@ -214,3 +214,14 @@ def random_gaussian_sketch(k: int, m: int, seed: int = 0) -> torch.Tensor:
         raise ValueError("need 1 <= k <= m")
     g = torch.Generator().manual_seed(int(seed) * 1_000_003 + 29)
     return (torch.randn(k, m, generator=g, dtype=torch.float64) / math.sqrt(k)).to(torch.float32)
+
+
+# Start block of the matrix-free (randomized block Krylov) sketch, SURVEY.md §8(f) f4: the random
+# numbers that method draws, passed in as an input so the GPU path and the oracle start alike.
+
+def start_block(m: int, p: int, seed: int = 0) -> torch.Tensor:
+    """[m][p] fp64 with i.i.d. N(0, 1) entries."""
+    if m < 1 or p < 1:
+        raise ValueError("need m, p >= 1")
+    g = torch.Generator().manual_seed(int(seed) * 1_000_003 + 41)
+    return torch.randn(m, p, generator=g, dtype=torch.float64)

@@ -17,6 +17,10 @@ numbers, "P:NNN"):
 * ``scw.scw_error``           ||A - SCW(A, S, r)||_F, dense residual
 * ``scw.best_rank_r_error``   ||A - [A]_r||_F  (Eckart-Young, P:26)
 * ``scw.test_error``          the paper's test-error metric
+* ``tucker2``                 the two-sided variant (Algorithm 5): mode-2 Gram, HOOI,
+                              two-sided SCW
+* ``matrix_free``             the Tucker1 sketch by randomized block Krylov without forming G
+                              (readings mf1-mf4 in DESIGN.md)
 * ``validators``              Theorem 1 and Theorem 2 checks
 
 Everything is numpy float64 with LAPACK/BLAS library primitives (matmul, eigh,
@@ -30,4 +34,4 @@ k = m, Theorems 1 and 2, SPEC worked examples (tests/golden/).  No function here
 "parity unpinned" except the paper's dataset-bound Table 2 numbers, which this
 oracle does not reproduce (datasets missing).
 """
-from . import tucker1, scw, validators  # noqa: F401
+from . import tucker1, scw, validators, tucker2, matrix_free  # noqa: F401
