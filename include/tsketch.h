@@ -168,6 +168,44 @@ tsk_status sketch_apply_two_sided_scw(tsk_ctx ctx, const float* A, int64_t B, in
 tsk_status two_sided_scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
                                const float* W, int l, int r, double* err);
 
+/* ---------------------------------------------------------------------- matrix-free sketch */
+/* the Tucker1 sketch approximated by randomized block
+   Krylov on A_(1) without forming the m x m Gram -- the pass-efficient direction the paper names as
+   future work.  Not the paper's algorithm: readings mf1-mf4 in DESIGN.md.  DEVICE pointers
+   only (TSK_EINVAL for host memory).
+     Q_0 = orth(Omega);  for j = 1..q: Y_j = sum_d A_d (A_d^T Q_{j-1}),
+       Krylov (default): Y_j -= sum_{i<j} Q_i Q_i^T Y_j (twice), Q_j = orth(Y_j), K = [Q_0|...|Q_q]
+       subspace:         Q_j = orth(Y_j), K = Q_q
+     Rayleigh-Ritz: Z_d = A_d^T K, H = sum_d Z_d^T Z_d = K^T G K, (theta, W) = eig(H) decreasing,
+     S = (K W_k)^T (sign rule c5), lambda = theta_1..theta_k.
+   Cost: 2q + 1 passes over A (3xTF32 tensor-core products), no m x m matrix.  The result is an
+   approximation of the exact sketch: Ritz values satisfy theta_i <= lambda_i(G) (interlacing) and
+   converge to them as q grows, at a rate set by the gap at k.
+   orth() is fp64 CholQR2; on breakdown (a block numerically dependent on the previous ones) the
+   dependent directions are replaced by pseudo-random ones orthogonal to K (reading mf3). */
+typedef struct {
+  int oversample;       /* block width p = k + oversample, rounded up to a multiple of 4, <= m;
+                           default (<= 0): 16 */
+  int power_iters;      /* q >= 0; default (< 0): the largest q <= 2 with width <= min(m, 256) */
+  int subspace;         /* 1: plain subspace iteration (K = Q_q); 0 (default): block Krylov */
+  const double* omega;  /* optional DEVICE [m][p] fp64 start block (p as above); NULL = deterministic
+                           pseudo-random uniform(-1, 1) block */
+} tsk_mf_opts;
+
+typedef struct {
+  int block;            /* p */
+  int power_iters;      /* q used */
+  int width;            /* columns of K: (q + 1) p (Krylov) or p (subspace) */
+  int passes;           /* passes over the training stack: 2 q + 1 */
+  int repairs;          /* blocks completed with pseudo-random directions (breakdown) */
+  double kyfan;         /* sum_{i<k} theta_i = tr(S G S^T) */
+} tsk_mf_info;
+
+/* A [D][m][n] fp32 (n % 4 == 0); S [k][m] fp32 (orthonormal rows, decreasing theta); lambda [k] fp64
+   (may be NULL).  Requires 1 <= k <= p and width <= min(m, 256) (TSK_EINVAL otherwise). */
+tsk_status sketch_train_matrix_free(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S,
+                                    double* lambda, const tsk_mf_opts* opts, tsk_mf_info* info);
+
 /* ---------------------------------------------------------------------- diagnostics */
 
 /* Diagnostic entry to the Gram kernel (tests / microbenchmarks only; not part of the method):

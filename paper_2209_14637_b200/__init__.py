@@ -32,7 +32,7 @@ STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVER
 EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_status_string", "tsk_launch_count",
             "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2",
             "sketch_train_two_sided", "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe",
-            "tsk_eig_probe"]
+            "tsk_eig_probe", "sketch_train_matrix_free"]
 
 
 class TskError(RuntimeError):
@@ -68,6 +68,19 @@ class HooiInfo(ctypes.Structure):
                 "residual_history": [self.residual_history[i] for i in range(self.sweeps + 1)]}
 
 
+class MfOpts(ctypes.Structure):
+    _fields_ = [("oversample", ctypes.c_int), ("power_iters", ctypes.c_int), ("subspace", ctypes.c_int),
+                ("omega", ctypes.c_void_p)]
+
+
+class MfInfo(ctypes.Structure):
+    _fields_ = [("block", ctypes.c_int), ("power_iters", ctypes.c_int), ("width", ctypes.c_int),
+                ("passes", ctypes.c_int), ("repairs", ctypes.c_int), ("kyfan", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 _lib: Optional[ctypes.CDLL] = None
 
 
@@ -100,9 +113,11 @@ def lib() -> ctypes.CDLL:
         L.two_sided_scw_error.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, f32p, i32, i32, f64p]
         L.tsk_gram_probe.argtypes = [vp, f32p, i64, i32, i32, f64p, i32, i32, i32]
         L.tsk_eig_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp]
+        L.sketch_train_matrix_free.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, vp, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
                   "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2", "sketch_train_two_sided",
-                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe"):
+                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe",
+                  "sketch_train_matrix_free"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -371,6 +386,26 @@ def two_sided_scw_error(A: torch.Tensor, S: torch.Tensor, W: torch.Tensor, r: in
     _check(lib().two_sided_scw_error(ctx.handle, _ptr(A), B, m, n, _ptr(S), S.shape[0], _ptr(W), W.shape[0], r,
                                      _ptr(err)), "two_sided_scw_error")
     return err
+
+
+def sketch_train_matrix_free(A: torch.Tensor, k: int, oversample: int = 0, power_iters: int = -1,
+                             subspace: bool = False, omega: Optional[torch.Tensor] = None,
+                             ctx: Optional[Context] = None):
+    """Matrix-free Tucker1 sketch by randomized block Krylov: returns (S [k][m],
+    lambda [k] fp64 Ritz values, info dict, status).  omega: optional [m][p] fp64 start block with
+    p = k + oversample rounded up to a multiple of 4 (capped at m)."""
+    _need(A, torch.float32, "A", 3)
+    D, m, n = A.shape
+    ctx = ctx or context(A.device)
+    S = torch.empty((k, m), dtype=torch.float32, device=A.device)
+    lam = torch.empty((k,), dtype=torch.float64, device=A.device)
+    if omega is not None:
+        _need(omega, torch.float64, "omega", 2)
+    o = MfOpts(oversample, power_iters, int(bool(subspace)), _ptr(omega))
+    info = MfInfo()
+    st = _check(lib().sketch_train_matrix_free(ctx.handle, _ptr(A), D, m, n, k, _ptr(S), _ptr(lam), ctypes.byref(o),
+                                               ctypes.byref(info)), "sketch_train_matrix_free")
+    return S, lam, info.as_dict(), st
 
 
 from .dist import shard_range, train  # noqa: E402,F401

@@ -453,6 +453,21 @@ tsk_status sketch_train_two_sided(tsk_ctx ctx, const float* A, int64_t D, int m,
   return tsk::hooi_tucker2(&ctx->c, A, D, m, n, k, l, S, W, opts, info);
 }
 
+// ------------------------------------------------------------------------------ matrix-free sketch
+// (device pointers only)
+tsk_status sketch_train_matrix_free(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S,
+                                    double* lambda, const tsk_mf_opts* opts, tsk_mf_info* info) {
+  if (!ctx) return TSK_ENULL;
+  if (!A || !S) return TSK_ENULL;
+  if (D < 1 || m < 1 || n < 1 || k < 1 || k > m) return TSK_EINVAL;
+  if (n % 4) return TSK_ESHAPE;
+  if (!is_device_ptr(A) || !is_device_ptr(S) || (lambda && !is_device_ptr(lambda)) ||
+      (opts && opts->omega && !is_device_ptr(opts->omega)))
+    return TSK_EINVAL;
+  cudaSetDevice(ctx->c.device);
+  return tsk::matrix_free_sketch(&ctx->c, A, D, m, n, k, S, lambda, opts, info);
+}
+
 static tsk_status scw2_common(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
                               const float* W, int l, int r, float* L, float* R, float* sigma, double* err) {
   if (!ctx) return TSK_ENULL;

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "dense64.cuh"
+#include "eig_kernels.cuh"
 #include "ptx.cuh"
 #include "tsk_internal.h"
 
@@ -232,7 +233,7 @@ static tsk_status cholqr1(Ctx* ctx, const double* Y, double* Q, int m, int p, do
   return cholqr_pass(ctx, Y, Q, m, p, C, R, flags);
 }
 
-static tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int m, int p, double* C, double* R,
+tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int m, int p, double* C, double* R,
                           int* flags) {
   tsk_status st;
   if ((st = cholqr_pass(ctx, Y, Q1, m, p, C, R, flags)) != TSK_OK) return st;
@@ -241,12 +242,23 @@ static tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int 
 
 tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
                       const tsk_train_opts* o, tsk_train_info* info) {
+  return topk_eigen_ex(ctx, G64, m, k, S, lambda, o, info, 0, nullptr);
+}
+
+// f64_products: G Q in fp64 (SIMT GEMM on the fp64 master copy) instead of 3xTF32 -- for small
+// dense matrices (the matrix-free sketch's Rayleigh-Ritz matrix, m <= 256) where fp64 is cheap and
+// the one-CTA Jacobi would have to leave shared memory (m > 116); tolerances scale accordingly.
+// X64 (optional, device [m][k] fp64): the output eigenvectors as columns, before the fp32 rounding
+// of S (same order; sign rule applied to S only).
+tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
+                         const tsk_train_opts* o, tsk_train_info* info, int f64_products, double* X64) {
   if (m < 1 || k < 1 || k > m) return TSK_EINVAL;
   tsk_train_opts opt{};
   if (o) opt = *o;
-  const int dense_max = opt.dense_max_m > 0 ? opt.dense_max_m : 256;
+  const bool f64 = f64_products != 0;
+  const int dense_max = opt.dense_max_m > 0 ? opt.dense_max_m : (f64 ? 116 : 256);
   const int max_iters = opt.max_iters > 0 ? opt.max_iters : 300;
-  const double tol = opt.tol > 0 ? opt.tol : 5e-7;
+  const double tol = opt.tol > 0 ? opt.tol : (f64 ? 1e-11 : 5e-7);
 
   // block size p = k + 16 by default: measured on C3/C4 spectra (flat near k), larger blocks cut
   // iterations less than they raise the cost of each p x p Rayleigh-Ritz solve
@@ -255,7 +267,7 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
   cudaStream_t s = ctx->stream;
   tsk_status st;
 
-  if (m <= dense_max || p >= m || m <= 256) {
+  if (m <= dense_max || p >= m || (!f64 && m <= 256)) {
     if (m > 256) return TSK_EINVAL;
     double* W = reinterpret_cast<double*>(ctx->workspace(WS_EIG_A, (size_t)m * m * 8));
     double* lam = reinterpret_cast<double*>(ctx->workspace(WS_EIG_SMALL, (size_t)m * 8 + 64));
@@ -263,6 +275,10 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
     if ((st = jacobi_eig_batched(ctx, G64, m, 1, W, lam)) != TSK_OK) return st;
     write_sketch_kernel<<<k, 256, 0, s>>>(W, m, m, S);
     ctx->count_launch();
+    if (X64) {
+      copy_cols_kernel<<<nblk((long long)m * k, 256), 256, 0, s>>>(W, m, 0, X64, k, 0, m, k);
+      ctx->count_launch();
+    }
     if (lambda) cudaMemcpyAsync(lambda, lam, (size_t)k * 8, cudaMemcpyDeviceToDevice, s);
     if (info) {
       info->iters = 0;
@@ -333,6 +349,7 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
 
   // Z = G' B for an m x pa fp64 block B (fp32 copy for the tensor cores; B <- fp64(fp32(B)))
   auto gq = [&](double* B, int pa) -> tsk_status {
+    if (f64) return gemm_nn_f64(ctx, Gd, m, 0, B, pa, 0, m, m, pa, 1, nullptr, Z, pa, 0);
     q_to_f32t_kernel<<<nblk((long long)pa * ms, 256), 256, 0, s>>>(B, m, pa, ms, Qt);
     ctx->count_launch();
     gp.N = pa;
@@ -378,7 +395,8 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
     max_res = 0.0;
     for (int c = 0; c < kr; ++c) max_res = std::max(max_res, hres[c]);
     max_res /= theta_top > 0 ? theta_top : 1.0;
-    const double tol_eff = std::max(tol, theta_top > 0 ? 4e-8 * gfro / theta_top : tol);
+    const double floor_rel = f64 ? 1e-14 : 4e-8;  // working-precision floor of the G Q products
+    const double tol_eff = std::max(tol, theta_top > 0 ? floor_rel * gfro / theta_top : tol);
     double kf_now = 0.0;  // Ky Fan energy of the current k wanted values (locked + active)
     {
       std::vector<double> hl(nl);
@@ -488,6 +506,7 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
   }
   write_sketch_kernel<<<k, 256, 0, s>>>(Xo, m, k, S);
   ctx->count_launch();
+  if (X64) cudaMemcpyAsync(X64, Xo, (size_t)m * k * 8, cudaMemcpyDeviceToDevice, s);
   if (lambda) {
     if (nl > 0) cudaMemcpyAsync(lambda, thl, (size_t)nl * 8, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(lambda + nl, theta, (size_t)kr * 8, cudaMemcpyDeviceToDevice, s);

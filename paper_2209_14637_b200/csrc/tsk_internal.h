@@ -50,6 +50,12 @@ enum WorkspaceId {
   WS_SCW2_0,       // two-sided SCW scratch
   WS_SCW2_1,
   WS_SCW2_2,
+  WS_MF_K,         // matrix-free sketch: Krylov blocks [nb][m][p] fp64
+  WS_MF_Y,         // matrix-free sketch: product / temporaries (fp64)
+  WS_MF_Z,         // matrix-free sketch: A_d^T K stack (fp32)
+  WS_MF_Q32,       // matrix-free sketch: K^T (fp32, tensor-core operand)
+  WS_MF_SMALL,     // matrix-free sketch: small fp64 matrices, flags
+  WS_MF_SCR,       // matrix-free sketch: fp64 GEMM split scratch
   WS_COUNT
 };
 
@@ -163,9 +169,16 @@ tsk_status hooi_tucker2(Ctx* ctx, const float* A, long long D, int m, int n, int
 tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, const float* W, int l,
                     int r, float* L, float* R, float* sigma, double* err);
 
+// matrix-free Tucker1 sketch by randomized block Krylov (matrix_free.cu), device pointers
+tsk_status matrix_free_sketch(Ctx* ctx, const float* A, long long D, int m, int n, int k, float* S, double* lambda,
+                              const tsk_mf_opts* o, tsk_mf_info* info);
+
 // eigensolver (eig.cu)
 tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda, const tsk_train_opts* o,
                       tsk_train_info* info);
+// f64_products: fp64 G Q products (small m); X64 (optional): the eigenvectors [m][k] fp64, columns
+tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
+                         const tsk_train_opts* o, tsk_train_info* info, int f64_products, double* X64);
 
 // SCW (scw.cu); all pointers device
 tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, int r, float* L,
