@@ -371,12 +371,36 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
   bool converged = false;
   double max_res = 0.0, kyfan = 0.0, theta_top = 0.0;
   int repairs = 0;
+  if (!opt.init_S) {
+    // One plain power step from the random start before the first Rayleigh-Ritz: the Ritz pairs of
+    // a random block are not worth a p x p eigensolve (C4: 7 Jacobi sweeps).  G Q's columns are all
+    // pulled toward x_1 (cond ~ lambda_1 / lambda_p, 2.5e4 at C4), well within CholQR2's fp64 reach;
+    // if it breaks down anyway (extreme spectra) the random block is kept.
+    cudaMemcpyAsync(Y0, Q, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
+    if ((st = gq(Q, pa)) != TSK_OK) return st;
+    ++products;
+    cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
+    if ((st = cholqr2(ctx, Z, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
+    int hf[2] = {0, 0};
+    if (cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return TSK_ECUDA;
+    if (hf[0] | hf[1]) {
+      cudaMemcpyAsync(Q, Y0, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
+      cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
+    }
+  }
   for (outer = 1; outer <= max_iters; ++outer) {
     const int kr = k - nl;  // wanted pairs still active
     if ((st = gq(Q, pa)) != TSK_OK) return st;
     ++products;
     if ((st = gemm_tn_f64(ctx, Q, pa, 0, Z, pa, 0, m, pa, pa, 1, H, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
-    if ((st = jacobi_eig_batched(ctx, H, pa, 1, W, theta, flags + 2, 1e-9)) != TSK_OK) return st;
+    // Rayleigh-Ritz accuracy follows the iteration: a Jacobi threshold tau leaves the Ritz vectors
+    // mixed by ~tau, which inflates their residuals by ~tau theta and leaves span(Q) unchanged, so
+    // tau = 0.1 x the previous max residual (1e-3 on the first, random, block) costs nothing in
+    // convergence, and the residual test below measures the vectors actually produced.
+    const double tol_rr = outer == 1 ? 1e-3 : std::max(f64 ? 1e-12 : 1e-9, std::min(1e-3, 0.1 * max_res));
+    if ((st = jacobi_eig_batched(ctx, H, pa, 1, W, theta, flags + 2, tol_rr)) != TSK_OK) return st;
     inv_theta_kernel<<<nblk(pa, 128), 128, 0, s>>>(theta, pa, invt);
     ctx->count_launch();
     if ((st = gemm_nn_f64(ctx, Z, pa, 0, W, pa, 0, m, pa, pa, 1, invt, Y, pa, 0)) != TSK_OK) return st;  // G'X/theta
@@ -412,8 +436,8 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     kyfan_prev = kf_now;
     if (getenv("TSK_EIG_TRACE"))
       fprintf(stderr, "[eig] outer=%d products=%d locked=%d max_res=%.3e (tol %.2e) theta0=%.4e theta_k=%.4e theta_p=%.4e "
-              "kyfan=%.12e rr_sweeps=%d\n", outer, products, nl, max_res, tol_eff, hth[0], hth[kr - 1], hth[pa - 1], kf_now,
-              hflags[2]);
+              "kyfan=%.12e rr_sweeps=%d res0=%.3e cholqr_flags=%d,%d\n", outer, products, nl, max_res, tol_eff, hth[0],
+              hth[kr - 1], hth[pa - 1], kf_now, hflags[2], hres[0] / theta_top, hflags[0], hflags[1]);
     if (hflags[0] + hflags[1] > 0) {
       // rank-deficient block (rank(G) < p): perturb with fresh directions and re-orthonormalise
       if (++repairs > 8) return TSK_ECUDA;
@@ -445,13 +469,19 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     const int pn = pa - off;
     // ---- Chebyshev filter on [0, b] applied to the remaining Ritz vectors X[:, off:pa]
     const double b = hth[pa - 1];
-    const double xmax = 2.0 * hth[off] / b - 1.0;
+    // the filter's dynamic range is set by the top of the spectrum: after the first Rayleigh-Ritz
+    // step (random start) theta_0 can underestimate lambda_max by orders of magnitude (C4: 7.7e6 vs
+    // 1.04e9), and a filter designed on it overflows the block into one direction (CholQR breaks
+    // down); there the upper bound ||G||_F >= lambda_max is used instead
+    const double top = outer == 1 ? std::max(hth[off], gfro) : hth[off];
+    const double xmax = 2.0 * top / b - 1.0;
     int d = 1;
     if (b > 0.0 && xmax > 1.0 + 1e-12) {
       const double ach = acosh(xmax);
       d = (int)std::floor(std::log(2e6) / ach);  // T_d(x) ~ exp(d acosh x) / 2 <= 1e6
       d = std::max(1, std::min(d, 12));
     }
+    if (getenv("TSK_EIG_TRACE")) fprintf(stderr, "[eig]   lock %d, filter degree %d on [0, %.4e], x_max %.3e\n", nnew, d, b, xmax);
     copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(X, pa, off, Y0, pn, 0, m, pn);
     ctx->count_launch();
     if (d == 1) {

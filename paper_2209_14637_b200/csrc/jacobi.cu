@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(kJacThreads)
     A[i * ld + j] = 0.5 * (Hb[(size_t)i * p + j] + Hb[(size_t)j * p + i]);
     V[i * ld + j] = (i == j) ? 1.0 : 0.0;
   }
+  __syncthreads();  // the diagonal scan below reads entries other threads wrote
   if (tid == 0) {
     double am = 0.0;
     for (int i = 0; i < p; ++i) am = fmax(am, fabs(A[i * ld + i]));
