@@ -101,15 +101,18 @@ __global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles
 
 // ---------------------------------------------------------------- C = X X^T, register-tiled fp64
 // grid (tiles^2, batch): CTA (ta, tc) computes the 64 x 64 block rows [64 ta, +64) x cols [64 tc, +64)
-// of C[b] (k <= 128) for X_b fp32 [k][len]; 256 threads = 16 x 16, each a 4 x 4 block.  X chunks are
-// converted to fp64 once on their way into shared memory (exact), products accumulate in fp64.
+// of C[b] (k <= 128) for X_b fp32 [k][len]; 256 threads = 16 x 16, thread (ty, tx) owns rows
+// ty + 16 i and cols tx + 16 j (i, j < 4: conflict-free / broadcast shared reads).  X chunks of 32
+// columns are read row-contiguously (one 128-B line per warp load) and converted to fp64 on their
+// way into shared memory (exact), stored transposed with an odd pitch; products accumulate in fp64.
 // cross form (X2 != nullptr): C[b] = X_b X2_b^T (k x k2, no mirroring)
 __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __restrict__ X, int k, int len,
                                                               double* __restrict__ C, const float* __restrict__ X2,
                                                               int k2) {
   constexpr int KC = 32;
-  __shared__ __align__(16) double xa[KC][64];
-  __shared__ __align__(16) double xc[KC][64];
+  constexpr int P = 65;
+  __shared__ double xa[KC][P];
+  __shared__ double xc[KC][P];
   const int b = blockIdx.y;
   const bool cross = X2 != nullptr;
   const int kc = cross ? k2 : k;
@@ -119,30 +122,29 @@ __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __res
   const float* Xb = X + (size_t)b * k * len;
   const float* Xc = cross ? X2 + (size_t)b * k2 * len : Xb;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int lane = tid & 31, wrow = tid >> 5;  // fill: warp w reads rows w, w + 8, ... (32 columns each)
   double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
   for (int j0 = 0; j0 < len; j0 += KC) {
-    for (int e = tid; e < 64 * KC; e += 256) {
-      // consecutive threads: consecutive rows (conflict-free fp64 stores; the strided global reads
-      // of one 32-column chunk share sectors through L1)
-      const int r = e % 64, jj = e / 64;
+    const bool inj = j0 + lane < len;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = wrow + 8 * t;
       const int ra = ta * 64 + r, rc = tc * 64 + r;
-      const bool inj = j0 + jj < len;
-      xa[jj][r] = (ra < k && inj) ? (double)Xb[(size_t)ra * len + j0 + jj] : 0.0;
-      xc[jj][r] = (rc < kc && inj) ? (double)Xc[(size_t)rc * len + j0 + jj] : 0.0;
+      xa[lane][r] = (ra < k && inj) ? (double)Xb[(size_t)ra * len + j0 + lane] : 0.0;
+      xc[lane][r] = (rc < kc && inj) ? (double)Xc[(size_t)rc * len + j0 + lane] : 0.0;
     }
     __syncthreads();
 #pragma unroll 8
     for (int jj = 0; jj < KC; ++jj) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&xa[jj][ty * 4]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&xa[jj][ty * 4 + 2]);
-      const double2 c01 = *reinterpret_cast<const double2*>(&xc[jj][tx * 4]);
-      const double2 c23 = *reinterpret_cast<const double2*>(&xc[jj][tx * 4 + 2]);
-      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-      const double cv[4] = {c01.x, c01.y, c23.x, c23.y};
+      double av[4], cv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = xa[jj][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cv[j] = xc[jj][tx + 16 * j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -153,11 +155,11 @@ __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __res
   double* Cb = C + (size_t)b * k * kc;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int ra = ta * 64 + ty * 4 + i;
+    const int ra = ta * 64 + ty + 16 * i;
     if (ra >= k) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int rc = tc * 64 + tx * 4 + j;
+      const int rc = tc * 64 + tx + 16 * j;
       if (rc >= kc) continue;
       Cb[(size_t)ra * kc + rc] = acc[i][j];
       if (!cross) Cb[(size_t)rc * k + ra] = acc[i][j];
