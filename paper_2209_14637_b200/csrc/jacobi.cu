@@ -37,9 +37,11 @@ __device__ __forceinline__ void rr_pair(int r, int k, int pe, int& i, int& j) {
 }
 
 // One half-warp (16 lanes) per rotation pair.  Phase 1 (per pair, no barrier needed because
-// pairs are disjoint): lane 0 computes (c, s) from A_ii, A_jj, A_ij and the half-warp rotates
-// rows i and j.  Phase 2: the half-warp rotates columns i and j of A and of V.
-template <bool kSmem>
+// pairs are disjoint): every lane of the half-warp computes (c, s) from A_ii, A_jj, A_ij
+// (broadcast reads: no shuffles, no divergence) and the half-warp rotates rows i and j.  Phase 2:
+// the half-warp rotates columns i and j of A and of V.  NQ = ceil(p / 16) strided elements per
+// lane, unrolled; KQ = pairs per half-warp (1, or 2 when p > 128).
+template <bool kSmem, int NQ, int KQ>
 __global__ void __launch_bounds__(kJacThreads)
     jacobi_eig_kernel(const double* __restrict__ H, int p, double* __restrict__ W, double* __restrict__ lam,
                       double* __restrict__ gscratch, int max_sweeps, double tol, int* __restrict__ sweeps_out) {
@@ -54,7 +56,6 @@ __global__ void __launch_bounds__(kJacThreads)
   const double* Hb = H + (size_t)b * p * p;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int hw = tid >> 4, hl = tid & 15, nhw = nt >> 4;  // half-warp id / lane
-  const unsigned hmask = (tid & 16) ? 0xFFFF0000u : 0x0000FFFFu;
   const int npairs = pe / 2;
   __shared__ double amax_s;
 
@@ -71,77 +72,88 @@ __global__ void __launch_bounds__(kJacThreads)
   }
   __syncthreads();
   // absolute floor: off-diagonals below 1e-15 * max|A_ii| are rounding noise of the updates
-  const double floor_abs = 1e-15 * amax_s;
+  const double floor2 = (1e-15 * amax_s) * (1e-15 * amax_s);
+  const double tol2 = tol * tol;
 
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) rot_count = 0;
     __syncthreads();
     for (int r = 0; r < pe - 1; ++r) {
-      double cc[2], ss[2];  // parameters of the (at most 2) pairs this half-warp owns this round
+      double cc[KQ], ss[KQ];  // parameters of the pairs this half-warp owns this round
+      int ii[KQ], jj[KQ];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < KQ; ++q) {
         const int k = hw + q * nhw;
         cc[q] = 1.0;
         ss[q] = 0.0;
+        ii[q] = 0;
+        jj[q] = 0;
         if (k < npairs) {
           int i, j;
           rr_pair(r, k, pe, i, j);
+          ii[q] = i;
+          jj[q] = j;
           if (j < p) {
-            double c = 1.0, s = 0.0;
-            if (hl == 0) {
-              const double aii = A[i * ld + i], ajj = A[j * ld + j], aij = A[i * ld + j];
-              // |A_ij| > max(tol sqrt|A_ii A_jj|, floor), squared: no fp64 square root on the chain
-              if (aij * aij > fmax(tol * tol * fabs(aii * ajj), floor_abs * floor_abs)) {
-                // tan of the annihilating angle, in fp32 (the MUFU path; ~1e-7 relative).  Any t
-                // gives an exactly orthogonal fp64 rotation (c^2 + s^2 = 1 to fp64 rounding); the
-                // residual ~1e-7 A_ij it leaves is removed by the quadratically convergent sweeps.
-                const float tau = __fdividef((float)(ajj - aii), (float)(2.0 * aij));
-                const float tf = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
-                const double t = (double)tf;
-                const double x = 1.0 + t * t;
-                double y = (double)rsqrtf((float)x);  // c = x^-1/2: two fp64 Newton steps
-                y = y * (1.5 - 0.5 * x * y * y);
-                y = y * (1.5 - 0.5 * x * y * y);
-                c = y;
-                s = t * y;
-                rot_count = 1;  // benign race: every writer stores 1 (a shared atomic here serialised the round)
-              }
+            const double aii = A[i * ld + i], ajj = A[j * ld + j], aij = A[i * ld + j];
+            // |A_ij| > max(tol sqrt|A_ii A_jj|, floor), squared: no fp64 square root on the chain
+            if (aij * aij > fmax(tol2 * fabs(aii * ajj), floor2)) {
+              // tan of the annihilating angle, in fp32 (the MUFU path; ~1e-7 relative).  Any t
+              // gives an exactly orthogonal fp64 rotation (c^2 + s^2 = 1 to fp64 rounding); the
+              // residual ~1e-7 A_ij it leaves is removed by the quadratically convergent sweeps.
+              const float tau = __fdividef((float)(ajj - aii), (float)(2.0 * aij));
+              const float tf = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
+              const double t = (double)tf;
+              const double x = 1.0 + t * t;
+              double y = (double)rsqrtf((float)x);  // c = x^-1/2: two fp64 Newton steps
+              y = y * (1.5 - 0.5 * x * y * y);
+              y = y * (1.5 - 0.5 * x * y * y);
+              cc[q] = y;
+              ss[q] = t * y;
+              if (hl == 0) rot_count = 1;  // benign race: every writer stores 1
             }
-            c = __shfl_sync(hmask, c, 0, 16);
-            s = __shfl_sync(hmask, s, 0, 16);
-            cc[q] = c;
-            ss[q] = s;
-            if (s != 0.0) {
-              double* Ai = A + i * ld;
-              double* Aj = A + j * ld;
-              for (int x = hl; x < p; x += 16) {
-                const double ai = Ai[x], aj = Aj[x];
-                Ai[x] = c * ai - s * aj;
-                Aj[x] = s * ai + c * aj;
-              }
+          }
+        }
+      }
+      // all reads of this round's diagonal entries precede the row updates (rows i, j of other
+      // pairs are disjoint from this pair's, but A_ii / A_jj of THIS pair are rewritten below)
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) {
+        const double c = cc[q], s = ss[q];
+        if (s != 0.0) {
+          double* Ai = A + ii[q] * ld;
+          double* Aj = A + jj[q] * ld;
+#pragma unroll
+          for (int u = 0; u < NQ; ++u) {
+            const int x = hl + 16 * u;
+            if (x < p) {
+              const double ai = Ai[x], aj = Aj[x];
+              Ai[x] = c * ai - s * aj;
+              Aj[x] = s * ai + c * aj;
             }
           }
         }
       }
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int k = hw + q * nhw;
-        const double s = ss[q];
-        if (k >= npairs || s == 0.0) continue;
-        const double c = cc[q];
-        int i, j;
-        rr_pair(r, k, pe, i, j);
-        for (int x = hl; x < p; x += 16) {
-          double* Ax = A + x * ld;
-          double* Vx = V + x * ld;
-          const double ai = Ax[i], aj = Ax[j];
-          Ax[i] = c * ai - s * aj;
-          Ax[j] = s * ai + c * aj;
-          const double vi = Vx[i], vj = Vx[j];
-          Vx[i] = c * vi - s * vj;
-          Vx[j] = s * vi + c * vj;
+      for (int q = 0; q < KQ; ++q) {
+        const double c = cc[q], s = ss[q];
+        if (s == 0.0) continue;
+        const int i = ii[q], j = jj[q];
+#pragma unroll
+        for (int u = 0; u < NQ; ++u) {
+          const int x = hl + 16 * u;
+          if (x < p) {
+            double* Ax = A + x * ld;
+            double* Vx = V + x * ld;
+            const double ai = Ax[i], aj = Ax[j];
+            Ax[i] = c * ai - s * aj;
+            Ax[j] = s * ai + c * aj;
+            const double vi = Vx[i], vj = Vx[j];
+            Vx[i] = c * vi - s * vj;
+            Vx[j] = s * vi + c * vj;
+          }
         }
       }
       __syncthreads();
@@ -168,6 +180,17 @@ __global__ void __launch_bounds__(kJacThreads)
   }
 }
 
+template <bool kSmem, int NQ, int KQ>
+static void launch_jacobi(int batch, int threads, size_t smem, cudaStream_t st, const double* H, int p, double* W,
+                          double* lam, double* scratch, double tol, int* sweeps) {
+  static bool attr = false;
+  if (kSmem && !attr) {
+    cudaFuncSetAttribute(jacobi_eig_kernel<kSmem, NQ, KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kJacSmemMax);
+    attr = true;
+  }
+  jacobi_eig_kernel<kSmem, NQ, KQ><<<batch, threads, smem, st>>>(H, p, W, lam, scratch, 30, tol, sweeps);
+}
+
 tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps,
                               double tol) {
   if (p < 1 || p > 256 || batch < 0) return TSK_EINVAL;
@@ -180,21 +203,19 @@ tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, doubl
     if (!scratch) return TSK_ENOMEM;
   }
   const size_t smem = use_smem ? need : 0;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(jacobi_eig_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kJacSmemMax) !=
-        cudaSuccess)
-      return TSK_ECUDA;
-    attr = true;
-  }
   // Rotate while |A_ij| > tol sqrt(|A_ii A_jj|) (and above an absolute rounding floor); the
   // eigenvectors come out accurate to ~tol / relative gap.
   // one half-warp per pair: p/2 pairs -> 8 p threads (at most 2 pairs per half-warp at p = 256)
   const int threads = std::min(kJacThreads, std::max(64, ((p + 1) / 2 * 16 + 31) / 32 * 32));
-  if (use_smem)
-    jacobi_eig_kernel<true><<<batch, threads, smem, ctx->stream>>>(H, p, W, lam, nullptr, 30, tol, sweeps);
-  else
-    jacobi_eig_kernel<false><<<batch, threads, 0, ctx->stream>>>(H, p, W, lam, scratch, 30, tol, sweeps);
+  cudaStream_t st = ctx->stream;
+  if (use_smem) {
+    if (p <= 32) launch_jacobi<true, 2, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps);
+    else if (p <= 64) launch_jacobi<true, 4, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps);
+    else launch_jacobi<true, 8, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps);
+  } else {
+    if (p <= 128) launch_jacobi<false, 8, 1>(batch, threads, 0, st, H, p, W, lam, scratch, tol, sweeps);
+    else launch_jacobi<false, 16, 2>(batch, threads, 0, st, H, p, W, lam, scratch, tol, sweeps);
+  }
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   ctx->count_launch();
   return TSK_OK;
