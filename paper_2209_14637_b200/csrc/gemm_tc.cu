@@ -649,6 +649,61 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long q0, q1;
       unit_range(a, u, t, q0, q1);
       const long long nchains = (q1 - q0 + a.chain - 1) / a.chain;
+      if constexpr (!kN64) {
+        if (a.resA && nchains == 1) {
+          // residual epilogue (SCW error) with one accumulator drain per unit: this
+          // thread's A row segment (64 columns) is requested BEFORE the accumulator is waited for,
+          // so the loads overlap the unit's MMA instead of following the drain
+          int bi, bj;
+          tile_coords(a, t, bi, bj);
+          const int b = t / a.T0;
+          const int gr = bi * kBM + row;
+          const int nv = (has_cols && gr < a.Mv) ? min(64, min(a.bn - col0, a.Nv - (bj * a.bn + col0))) : 0;
+          const float* ar = a.resA + (size_t)b * a.res_stride + (size_t)(gr < a.Mv ? gr : 0) * a.res_ld +
+                            (size_t)bj * a.bn + col0;
+          float av[64];
+          if (nv == 64 && ((reinterpret_cast<uintptr_t>(ar) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 64; i += 4) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(ar + i));
+              av[i] = v.x;
+              av[i + 1] = v.y;
+              av[i + 2] = v.z;
+              av[i + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i) av[i] = i < nv ? __ldg(ar + i) : 0.f;
+          }
+          mbar_wait(&accf[ab], aph);
+          tc_fence_after();
+          const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)ab * kTsAccCols + col0;
+          double acc = 0.0;
+          if (has_cols) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(taddr + h * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                if (h * 32 + i < nv) {
+                  const double d = (double)av[h * 32 + i] - (double)__uint_as_float(r[i]);
+                  acc += d * d;
+                }
+              }
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acce[ab]);
+          if (++ab == 2) { ab = 0; aph ^= 1; }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) a.res_part[(size_t)u * 8 + e] = acc;
+          continue;
+        }
+      }
       float sum[64];
 #pragma unroll
       for (int i = 0; i < 64; ++i) sum[i] = 0.f;
