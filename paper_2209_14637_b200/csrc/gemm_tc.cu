@@ -429,30 +429,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto lo_ptr = [&](int st) { return lo_base + st * LB; };
 
   if (warp == 0) {
-    // ===================== TMA producer + drift throttle (as in the SS kernel) =====================
-    int st = 0;
-    uint32_t ph = 0;
-    for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-      int t, bi, bj;
-      long long q0, q1;
-      unit_range(a, u, t, q0, q1);
-      tile_coords(a, t, bi, bj);
-      const bool diag = a.sym && bi == bj;
-      const int s_split = u / a.T;
-      const int round = u / gridDim.x;
-      // lanes 0-3 issue the X boxes and lanes 4-7 the Y boxes of 4 consecutive chunks (a thread's TMA
-      // boxes complete one after another; scripts/tma_bench.cu); rfull expects both arrivals
+    // ===================== TMA producer + drift throttle =====================
+    // Lanes 0-3 issue the X boxes and lanes 4-7 the Y boxes; lane j (mod 4) owns the chunks whose
+    // CTA-wide index is j mod 4 and runs decoupled from the other lanes, each chunk issued as soon
+    // as its stage is free (a thread's TMA boxes complete one after another, scripts/tma_bench.cu,
+    // so one lane cannot keep the ring full; and lanes stepping in lock-step groups of 4 left at
+    // most one free stage of lead: SA/AV at C4 ran one chunk per 0.69 us against 0.21 us of MMA).
+    if (lane < 8) {
+      const int j = lane & 3;
+      const bool isx = lane < 4;
       const uint32_t ybytes = (uint32_t)(a.bn * kBK * 4);
-      for (long long qb = q0; qb < q1; qb += 4) {
-        const int j = lane & 3;
-        const long long q = qb + j;
-        if (lane < 8 && q < q1) {
-          const int sl = (st + j) % RS;
-          const uint32_t pl = ph ^ (uint32_t)(((st + j) / RS) & 1);
-          mbar_wait(&rempty[sl], pl ^ 1);
+      long long idx = 0;  // CTA-wide chunk index (stage = idx % RS, use = idx / RS)
+      for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        int t, bi, bj;
+        long long q0, q1;
+        unit_range(a, u, t, q0, q1);
+        tile_coords(a, t, bi, bj);
+        const bool diag = a.sym && bi == bj;
+        const int s_split = u / a.T;
+        const int round = u / gridDim.x;
+        // first chunk of this unit owned by this lane
+        long long q = q0 + ((((long long)j - idx) % 4) + 4) % 4;
+        long long ci = idx + (q - q0);
+        for (; q < q1; q += 4, ci += 4) {
+          const int sl = (int)(ci % RS);
+          const uint32_t use = (uint32_t)((ci / RS) & 1);
+          mbar_wait(&rempty[sl], use ^ 1);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
-          if (lane < 4) {
+          if (isx) {
             mbar_arrive_expect_tx(&rfull[sl], (uint32_t)kTileBytes);
             if (a.xt) tma_load_3d(raw_ptr(sl, 0), &mapX, &rfull[sl], bi * kBM, kc, z);  // box {128 M, 32 K}
             else tma_load_3d(raw_ptr(sl, 0), &mapX, &rfull[sl], kc, bi * kBM, z);
@@ -463,29 +468,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kYT) tma_load_3d(raw_ptr(sl, 1), &mapY, &rfull[sl], bj * a.bn, kc, a.ybc ? 0 : z);  // {bn N, 32 K}
             else tma_load_3d(raw_ptr(sl, 1), &mapY, &rfull[sl], kc, bj * a.bn, a.ybc ? 0 : z);   // {32 K, bn N}
           }
-        }
-        __syncwarp();
-        const int nq = (int)min(4LL, q1 - qb);
-        ph ^= (uint32_t)(((st + nq) / RS) & 1);
-        st = (st + nq) % RS;
-        const unsigned done = (unsigned)(qb - q0 + nq);
-        if (a.lag > 0 && ((done & 31u) == 0 || qb + nq == q1)) {
-          if (lane == 0) st_volatile_u32(&a.progress[u], qb + nq == q1 ? 0xFFFFFFFFu : done);
-          if (qb + nq < q1) {
+          // drift throttle (lane 0 alone; the other lanes are bounded by the ring): units of the
+          // same K window in the same round read the same operands through L2
+          const unsigned done = (unsigned)(q - q0 + 1);
+          if (lane == 0 && a.lag > 0 && (done & 31u) < 4u && q + 4 < q1) {
+            st_volatile_u32(&a.progress[u], done);
             while (true) {
               unsigned mn = 0xFFFFFFFFu;
-              for (int tp = lane; tp < a.T; tp += 32) {
+              for (int tp = 0; tp < a.T; ++tp) {
                 const int up = s_split * a.T + tp;
                 if (up != u && up / (int)gridDim.x == round) mn = min(mn, ld_volatile_u32(&a.progress[up]));
               }
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
               if (mn == 0xFFFFFFFFu || done <= mn + (unsigned)a.lag) break;
               __nanosleep(1000);
             }
           }
         }
-        __syncwarp();
+        if (lane == 0 && a.lag > 0) st_volatile_u32(&a.progress[u], 0xFFFFFFFFu);
+        idx += q1 - q0;
       }
     }
   } else if (warp == 1) {
