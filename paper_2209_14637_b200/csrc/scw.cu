@@ -25,18 +25,20 @@ namespace tsk {
 // ---------------------------------------------------------------- fp64-coefficient combinations
 // Out_b[c][j] (kVt) or Out_b[j][c] = sc_c sum_{a<k} W_b[a][c] In_b[a][j],  c < nout, j < len
 // (kVt: V^T = L^{-1} P B with sc from mu; else the factors L = Z W_r, R = V W_r with sc = 1).
-// Thread per column j: its k inputs are read once into registers (fp32), each is converted to fp64
-// once per 16-wide block of outputs, and the 16 fp64 accumulators take the coefficients from shared
-// memory as broadcast reads.
+// Thread per two columns j: the 2 x 16 fp64 accumulators of a 16-wide block of outputs take the
+// coefficients from shared memory as broadcast double2 reads (row pitch ldn = nout rounded up to
+// even, 16 doubles of slack after the last row for the over-read of a partial block).
 template <int KMAX, bool kVt>
 __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restrict__ In, const double* __restrict__ W,
                                                           const double* __restrict__ mu, int k, int len, int nout,
                                                           int ldw, long long wst, float* __restrict__ Out, int ldo) {
-  extern __shared__ double wsm[];  // [k][nout] coefficients, then [nout] scales
+  extern __shared__ double wsm[];  // [k][ldn] coefficients, 16 slack, then [nout] scales
   const int b = blockIdx.y;
+  const int ldn = (nout + 1) & ~1;
   const double* Wb = W + (size_t)b * wst;
-  for (int e = threadIdx.x; e < k * nout; e += blockDim.x) wsm[e] = Wb[(size_t)(e / nout) * ldw + (e % nout)];
-  double* sc = wsm + (size_t)k * nout;
+  for (int e = threadIdx.x; e < k * nout; e += blockDim.x)
+    wsm[(size_t)(e / nout) * ldn + (e % nout)] = Wb[(size_t)(e / nout) * ldw + (e % nout)];
+  double* sc = wsm + (size_t)k * ldn + 16;
   for (int c = threadIdx.x; c < nout; c += blockDim.x) {
     if (kVt) {
       const double m0 = mu[(size_t)b * k];
@@ -47,40 +49,54 @@ __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restric
     }
   }
   __syncthreads();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= len) return;
+  // two columns per thread (j0, j0 + blockDim.x): every coefficient pair read from shared memory
+  // (one double2, a broadcast) feeds 4 DFMA -- one coefficient per DFMA made the kernel
+  // shared-memory-issue bound at half the fp64 rate
+  const int j0 = blockIdx.x * 2 * blockDim.x + threadIdx.x, j1 = j0 + blockDim.x;
+  if (j0 >= len) return;
+  const bool has1 = j1 < len;
   const float* Ib = In + (size_t)b * k * len;
-  constexpr bool kReg = false;  // inputs re-read through L1 per output block (registers for occupancy)
-  float iv[kReg ? KMAX : 1];
-  if (kReg) {
-#pragma unroll
-    for (int a = 0; a < (kReg ? KMAX : 1); ++a) iv[a] = a < k ? Ib[(size_t)a * len + j] : 0.f;
-  }
   float* Ob = Out + (size_t)b * (kVt ? (size_t)nout * len : (size_t)len * ldo);
   for (int c0 = 0; c0 < nout; c0 += 16) {
-    double s[16];
+    double s0[16], s1[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) s[q] = 0.0;
-#pragma unroll(kReg ? KMAX : 4)
+    for (int q = 0; q < 16; ++q) s0[q] = s1[q] = 0.0;
+#pragma unroll 4
     for (int a = 0; a < KMAX; ++a) {
       if (a < k) {
-        const double x = kReg ? (double)iv[kReg ? a : 0] : (double)Ib[(size_t)a * len + j];
-        const double* wr = wsm + (size_t)a * nout + c0;
+        const double x0 = (double)Ib[(size_t)a * len + j0];
+        const double x1 = has1 ? (double)Ib[(size_t)a * len + j1] : 0.0;
+        const double2* wr = reinterpret_cast<const double2*>(wsm + (size_t)a * ldn + c0);
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          if (c0 + q < nout) s[q] = fma(wr[q], x, s[q]);
+        for (int q = 0; q < 8; ++q) {
+          const double2 w = wr[q];
+          s0[2 * q] = fma(w.x, x0, s0[2 * q]);
+          s0[2 * q + 1] = fma(w.y, x0, s0[2 * q + 1]);
+          s1[2 * q] = fma(w.x, x1, s1[2 * q]);
+          s1[2 * q + 1] = fma(w.y, x1, s1[2 * q + 1]);
+        }
       }
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int c = c0 + q;
       if (c < nout) {
-        const float v = (float)(s[q] * sc[c]);
-        if (kVt) Ob[(size_t)c * len + j] = v;
-        else Ob[(size_t)j * ldo + c] = v;
+        const float v0 = (float)(s0[q] * sc[c]);
+        const float v1 = (float)(s1[q] * sc[c]);
+        if (kVt) {
+          Ob[(size_t)c * len + j0] = v0;
+          if (has1) Ob[(size_t)c * len + j1] = v1;
+        } else {
+          Ob[(size_t)j0 * ldo + c] = v0;
+          if (has1) Ob[(size_t)j1 * ldo + c] = v1;
+        }
       }
     }
   }
+}
+
+static inline size_t combine_smem(int k, int nout) {
+  return ((size_t)k * ((nout + 1) & ~1) + 16 + nout) * sizeof(double);
 }
 
 __global__ void scw_sigma_kernel(const double* __restrict__ sig2, int k, int r, long long B, float* __restrict__ sigma) {
@@ -427,8 +443,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) {
       return st;
     }
-    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
-    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
+    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 256), bc), 128, combine_smem(k, k), s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
+    else scw_combine_kernel<128, true><<<dim3(nb(n, 256), bc), 128, combine_smem(k, k), s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
     if ((st = launch_status("scw vt")) != TSK_OK) return st;
     // 3. Z^T = V^T A^T
     {
@@ -461,11 +477,11 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf;
     if (k <= 64) {
-      scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
-      scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
+      scw_combine_kernel<64, false><<<dim3(nb(m, 256), bc), 128, combine_smem(k, r), s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
+      scw_combine_kernel<64, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
     } else {
-      scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
-      scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
+      scw_combine_kernel<128, false><<<dim3(nb(m, 256), bc), 128, combine_smem(k, r), s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
+      scw_combine_kernel<128, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
     }
     ctx->count_launch(2);
     if (sigma) {
@@ -535,8 +551,8 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     }
     launch_gram_rows_tiled(Bm, k, n, bc, Cq, s);
     chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cq, k, Wq, muq);
-    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt, 0);
-    else scw_combine_kernel<128, true><<<dim3(nb(n, 128), bc), 128, (kk + k) * 8, s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt, 0);
+    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 256), bc), 128, combine_smem(k, k), s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt, 0);
+    else scw_combine_kernel<128, true><<<dim3(nb(n, 256), bc), 128, combine_smem(k, k), s>>>(Bm, Wq, muq, k, n, k, k, (long long)kk, Vt, 0);
     ctx->count_launch(3);
     if ((st = launch_status("scw2 Q")) != TSK_OK) return st;
     // 2. P^T: W A_b^T = (A_b W^T)^T (tcgen05, W broadcast, transposed store), same orthonormalisation
@@ -551,8 +567,8 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     }
     launch_gram_rows_tiled(Yt, l, m, bc, Cp, s);
     chol_basis_kernel<<<bc, 128, (size_t)2 * l * (l + 1) * 8, s>>>(Cp, l, Wp, mup);
-    if (l <= 64) scw_combine_kernel<64, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt, 0);
-    else scw_combine_kernel<128, true><<<dim3(nb(m, 128), bc), 128, (ll + l) * 8, s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt, 0);
+    if (l <= 64) scw_combine_kernel<64, true><<<dim3(nb(m, 256), bc), 128, combine_smem(l, l), s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt, 0);
+    else scw_combine_kernel<128, true><<<dim3(nb(m, 256), bc), 128, combine_smem(l, l), s>>>(Yt, Wp, mup, l, m, l, l, (long long)ll, Pt, 0);
     ctx->count_launch(3);
     if ((st = launch_status("scw2 P")) != TSK_OK) return st;
     // 3. A_b Q as Z^T = Q^T A_b^T (tcgen05), then M = P^T (A_b Q) as an fp64 cross Gram of rows
@@ -576,14 +592,14 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
     float* Lc = L ? L + (size_t)b0 * m * r : Lw;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf;
     if (k <= 64 && l <= 64) {
-      scw_combine_kernel<64, false><<<dim3(nb(m, 128), bc), 128, ((size_t)l * r + r) * 8, s>>>(Pt, CL, nullptr, l, m, r, r,
+      scw_combine_kernel<64, false><<<dim3(nb(m, 256), bc), 128, combine_smem(l, r), s>>>(Pt, CL, nullptr, l, m, r, r,
                                                                                  (long long)l * r, Lc, ldf);
-      scw_combine_kernel<64, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k,
+      scw_combine_kernel<64, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k,
                                                                                  (long long)kk, Rc, ldf);
     } else {
-      scw_combine_kernel<128, false><<<dim3(nb(m, 128), bc), 128, ((size_t)l * r + r) * 8, s>>>(Pt, CL, nullptr, l, m, r, r,
+      scw_combine_kernel<128, false><<<dim3(nb(m, 256), bc), 128, combine_smem(l, r), s>>>(Pt, CL, nullptr, l, m, r, r,
                                                                                   (long long)l * r, Lc, ldf);
-      scw_combine_kernel<128, false><<<dim3(nb(n, 128), bc), 128, ((size_t)k * r + r) * 8, s>>>(Vt, W2, nullptr, k, n, r, k,
+      scw_combine_kernel<128, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k,
                                                                                   (long long)kk, Rc, ldf);
     }
     ctx->count_launch(3);
