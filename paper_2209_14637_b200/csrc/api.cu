@@ -145,6 +145,9 @@ tsk_status tsk_destroy(tsk_ctx ctx) {
   for (int i = 0; i < tsk::WS_COUNT; ++i)
     if (c.ws[i]) cudaFree(c.ws[i]);
   if (c.host_pinned) cudaFreeHost(c.host_pinned);
+  if (c.side) cudaStreamDestroy(c.side);
+  for (auto& ev : c.ev)
+    if (ev) cudaEventDestroy(ev);
   CtxExt* e = ext_of(ctx);
   for (int i = 0; i < 2; ++i) {
     if (e->buf[i]) cudaFree(e->buf[i]);

@@ -383,30 +383,44 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
                    float* R, float* sigma, double* err) {
   if (B == 0) return TSK_OK;
   if (k > 128 || r > 64) return TSK_EINVAL;
-  cudaStream_t s = ctx->stream;
+  const cudaStream_t s0 = ctx->stream;
   const long long chunk = std::min<long long>(B, 512);
   const size_t kn = (size_t)k * n, km = (size_t)k * m, kk = (size_t)k * k;
-  float* Bm = reinterpret_cast<float*>(ctx->workspace(WS_SCW_0, chunk * kn * 4));
-  float* Vt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
-  float* Zt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
+  float* Bm_all = reinterpret_cast<float*>(ctx->workspace(WS_SCW_0, chunk * kn * 4));
+  float* Vt_all = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
+  float* Zt_all = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
   double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW_3, chunk * (4 * kk + 2 * k) * 8));
   const int tiles = (int)(nb(n, 128) * nb(m, 128)) * 8;  // residual partials per matrix
   // factor row pitch: r for the caller's L / R, r rounded up to 4 (16-byte TMA rows) for the error path
   const int ldf = (L || R) ? r : (r + 3) & ~3;
   float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * ldf * 4));
   double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
-  if (!Bm || !Vt || !Zt || !small || !Lw || !part) return TSK_ENOMEM;
-  double* Cb = small;
-  double* Wc = small + chunk * kk;
-  double* H = small + 2 * chunk * kk;
-  double* W2 = small + 3 * chunk * kk;
-  double* mu = small + 4 * chunk * kk;
-  double* sig2 = mu + chunk * k;
+  if (!Bm_all || !Vt_all || !Zt_all || !small || !Lw || !part) return TSK_ENOMEM;
+  double* Cb_all = small;
+  double* Wc_all = small + chunk * kk;
+  double* H_all = small + 2 * chunk * kk;
+  double* W2_all = small + 3 * chunk * kk;
+  double* mu_all = small + 4 * chunk * kk;
+  double* sig2_all = mu_all + chunk * k;
   scw_attrs();
-  tsk_status st;
-  for (long long b0 = 0; b0 < B; b0 += chunk) {
-    const int bc = (int)std::min(chunk, B - b0);
+  // Each chunk runs as two halves on two streams, the second started one phase (its SA product)
+  // behind the first, so the latency-bound small solves of one half (row Grams, pivoted Cholesky,
+  // batched Jacobi, factor combinations) overlap the HBM/tensor-bound products of the other.
+  const bool two = chunk >= 64 && k <= 116 && ctx->side_ready();
+  auto half = [&](long long b0, int bc, long long off0, cudaStream_t s, cudaEvent_t after_sa) -> tsk_status {
+    ctx->stream = s;
+    tsk_status st;
+    const size_t off = (size_t)off0;
     const float* Ac = A + (size_t)b0 * m * n;
+    float* Bm = Bm_all + off * kn;
+    float* Vt = Vt_all + off * kn;
+    float* Zt = Zt_all + off * km;
+    double* Cb = Cb_all + off * kk;
+    double* Wc = Wc_all + off * kk;
+    double* H = H_all + off * kk;
+    double* W2 = W2_all + off * kk;
+    double* mu = mu_all + off * k;
+    double* sig2 = sig2_all + off * k;
     // 1. B = S A on tcgen05 (3xTF32): (S A_b)^T = A_b^T S^T with X = A_b read transposed (the
     // contraction runs over the rows of A_b), Y = S broadcast to every matrix; one unit per
     // (matrix, 128-column tile of A_b), stored transposed as B [k][n]
@@ -431,6 +445,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       gp.ldd = n;
       if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
     }
+    if (after_sa) cudaEventRecord(after_sa, s);
     // 2. orthonormal row basis of B: fp64 Gram, pivoted Cholesky, V^T = L^{-1} P B (k > 116 does
     // not fit the factor and its inverse in shared memory: eigen-orthonormalisation instead)
     launch_gram_rows_tiled(Bm, k, n, bc, Cb, s);
@@ -474,8 +489,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     if ((st = launch_status("scw gram(AV)")) != TSK_OK) return st;
     if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10)) != TSK_OK) return st;
     // 5. factors
-    float* Lc = L ? L + (size_t)b0 * m * r : Lw;
-    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf;
+    float* Lc = L ? L + (size_t)b0 * m * r : Lw + (size_t)off * m * ldf;
+    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf + (size_t)off * n * ldf;
     if (k <= 64) {
       scw_combine_kernel<64, false><<<dim3(nb(m, 256), bc), 128, combine_smem(k, r), s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
       scw_combine_kernel<64, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
@@ -489,12 +504,33 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       ctx->count_launch();
     }
     // 6. dense residual (the error path always has pitch-aligned workspace factors)
-    if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part, err + b0)) != TSK_OK) return st;
+    if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part + (size_t)off * tiles, err + b0)) != TSK_OK) return st;
     if ((st = launch_status("scw")) != TSK_OK) return st;
+    return TSK_OK;
+  };
+  for (long long b0 = 0; b0 < B; b0 += chunk) {
+    const int bc = (int)std::min(chunk, B - b0);
+    tsk_status st;
+    if (two && bc >= 64) {
+      const int h0 = bc / 2;
+      cudaEventRecord(ctx->ev[0], s0);  // fork: the side stream starts after the work before this call
+      cudaStreamWaitEvent(ctx->side, ctx->ev[0], 0);
+      st = half(b0, h0, 0, s0, ctx->ev[1]);
+      if (st == TSK_OK) {
+        cudaStreamWaitEvent(ctx->side, ctx->ev[1], 0);
+        st = half(b0 + h0, bc - h0, h0, ctx->side, nullptr);
+      }
+      ctx->stream = s0;
+      cudaEventRecord(ctx->ev[2], ctx->side);  // join
+      cudaStreamWaitEvent(s0, ctx->ev[2], 0);
+    } else {
+      st = half(b0, bc, 0, s0, nullptr);
+      ctx->stream = s0;
+    }
+    if (st != TSK_OK) return st;
   }
   return TSK_OK;
 }
-
 
 // Two-sided SCW (Algorithm 3) for a batch of test matrices:
 //   1. Q^T = orthonormal basis of rowspace(S A_b)    (k x n; as steps 1-2 of SCW)

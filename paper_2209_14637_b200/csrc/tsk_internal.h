@@ -106,6 +106,24 @@ struct Ctx {
     return host_pinned;
   }
   void count_launch(int n = 1) { launches += n; }
+  // side stream + fork/join events (batched SCW runs two halves of a chunk concurrently), created on
+  // first use and destroyed with the ctx
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  bool side_ready() {
+    if (side) return true;
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) {
+      side = nullptr;
+      cudaGetLastError();
+      return false;
+    }
+    for (auto& e : ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+    return true;
+  }
   // pair-Gram schedule last uploaded to ws[WS_GRAM_SCHED] (pointer + host schedule version)
   const void* gram_sched_dev = nullptr;
   long long gram_sched_ver = -1;
