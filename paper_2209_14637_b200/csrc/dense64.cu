@@ -325,11 +325,11 @@ __global__ void __launch_bounds__(256) chol_inv2_kernel(const double* __restrict
 tsk_status chol_inv2(Ctx* ctx, const double* C, int p, int batch, double rel_tol, double* Rinv, int* flag) {
   const size_t smem = (size_t)2 * p * (p | 1) * sizeof(double);
   if (smem > 220 * 1024 || p > 128) return TSK_EINVAL;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
     if (cudaFuncSetAttribute(chol_inv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) != cudaSuccess)
       return TSK_ECUDA;
-    attr = true;
+    attr |= device_bit();
   }
   chol_inv2_kernel<<<batch, 256, smem, ctx->stream>>>(C, p, rel_tol, Rinv, flag);
   ctx->count_launch();
@@ -344,12 +344,12 @@ tsk_status chol(Ctx* ctx, const double* C, int p, int batch, double rel_tol, dou
     scratch = reinterpret_cast<double*>(ctx->workspace(ws_id, need * batch));
     if (!scratch) return TSK_ENOMEM;
   }
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
     if (cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(trsm_rlt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) != cudaSuccess)
       return TSK_ECUDA;
-    attr = true;
+    attr |= device_bit();
   }
   chol_kernel<<<batch, kCholThreads, use_smem ? need : 0, ctx->stream>>>(C, p, rel_tol, L, flag, scratch, use_smem);
   ctx->count_launch();

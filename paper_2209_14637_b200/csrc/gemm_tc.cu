@@ -1017,8 +1017,8 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   if (cudaMemsetAsync(prog, 0, (size_t)a.U * sizeof(unsigned), ctx->stream) != cudaSuccess) return TSK_ECUDA;
 
   constexpr int kTsYtSmemBytes = ((kRawStages - 1) * 2 + 2 * kTsLoStages) * kTileBytes + 1024 + 256;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;
+  if (!(attr_set & device_bit())) {
     if (cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
             cudaSuccess ||
         cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1030,7 +1030,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
         cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kTsYtSmemBytes) != cudaSuccess)
       return TSK_ECUDA;
-    attr_set = true;
+    attr_set |= device_bit();
   }
   const int grid = std::min(a.U, ctx->num_sms);
   // production: TS variant (A operand from TMEM); the SS variant serves the diagnostic modes

@@ -602,14 +602,14 @@ tsk_status gram_pair(Ctx* ctx, const GemmProblem& p) {
       !map3d(&my32, p.X, p.n, m, p.D, p.x_row_stride, p.x_slice_stride, 32, kZ))
     return TSK_ECUDA;
 
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
     if (cudaFuncSetAttribute(gram_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
             cudaSuccess ||
         cudaFuncSetAttribute(gram_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
             cudaSuccess)
       return TSK_ECUDA;
-    attr = true;
+    attr |= device_bit();
   }
   // persistent clusters: no more than can be co-resident (the drift throttle assumes every unit of
   // a round is running)

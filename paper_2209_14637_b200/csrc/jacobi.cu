@@ -183,10 +183,10 @@ __global__ void __launch_bounds__(kJacThreads)
 template <bool kSmem, int NQ, int KQ>
 static void launch_jacobi(int batch, int threads, size_t smem, cudaStream_t st, const double* H, int p, double* W,
                           double* lam, double* scratch, double tol, int* sweeps) {
-  static bool attr = false;
-  if (kSmem && !attr) {
+  static uint64_t attr = 0;
+  if (kSmem && !(attr & device_bit())) {
     cudaFuncSetAttribute(jacobi_eig_kernel<kSmem, NQ, KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kJacSmemMax);
-    attr = true;
+    attr |= device_bit();
   }
   jacobi_eig_kernel<kSmem, NQ, KQ><<<batch, threads, smem, st>>>(H, p, W, lam, scratch, 30, tol, sweeps);
 }

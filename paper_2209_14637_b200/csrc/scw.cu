@@ -368,14 +368,14 @@ static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, c
 }
 
 static void scw_attrs() {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
     cudaFuncSetAttribute(scw_combine_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
-    attr = true;
+    attr |= device_bit();
   }
 }
 

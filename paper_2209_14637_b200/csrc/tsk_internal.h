@@ -22,6 +22,14 @@ inline tsk_status launch_status(const char* where) {
   return TSK_ECUDA;
 }
 
+// one bit per device: kernel attributes (dynamic shared memory limits) are per device, so the
+// "set once" flags of the launch helpers are kept per device
+inline uint64_t device_bit() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return 1ull << (d & 63);
+}
+
 enum WorkspaceId {
   WS_GEMM_PARTIAL = 0,
   WS_EIG_A,      // fp64 m x p blocks
