@@ -87,7 +87,8 @@ struct Ctx {
     if (bytes == 0) bytes = 16;
     if (ws_size[id] >= bytes) return ws[id];
     if (ws[id]) {
-      cudaStreamSynchronize(stream);
+      // the old buffer may be in use on this ctx's stream or its side stream (batched SCW)
+      cudaDeviceSynchronize();
       cudaFree(ws[id]);
       ws[id] = nullptr;
       ws_size[id] = 0;
