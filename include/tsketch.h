@@ -49,6 +49,7 @@ typedef enum {
   TSK_ESHAPE = -2,            /* n % 4 != 0, misaligned pointer */
   TSK_ENOMEM = -3,            /* device workspace allocation failed */
   TSK_ECUDA = -4,             /* CUDA runtime / launch / device fault */
+  TSK_ENCCL = -5,             /* NCCL library not loadable, or an NCCL call failed */
   TSK_EDEVICE = -6,           /* device is not compute capability 10.0 (sm_100a) */
   TSK_ENULL = -8              /* a required pointer is NULL */
 } tsk_status;
@@ -64,6 +65,20 @@ tsk_status tsk_sync(tsk_ctx ctx);
 const char* tsk_status_string(tsk_status s);
 /* Number of kernels this ctx has launched since creation (bench evidence). */
 int64_t tsk_launch_count(tsk_ctx ctx);
+
+/* ---------------------------------------------------------------------- multi-GPU */
+/* one process per GPU; the training stream is sharded by matrix index (rank p owns
+   the contiguous range [floor(pD/P), floor((p+1)D/P))), each rank accumulates its local Gram and ONE
+   all-reduce (sum, fp64) of the m x m Gram over NVLink/NVSwitch gives G on every rank; every rank then
+   runs the same deterministic eigensolver (identical S, no broadcast).  NCCL is loaded at run time
+   (libnccl.so.2, reusing the copy already in the process if any): TSK_ENCCL if it is not available.
+   tsk_get_unique_id: uid[128] (host memory) to be broadcast by the caller (e.g. over torch.distributed).
+   tsk_comm_init: collective over the nranks processes (same uid, distinct rank in [0, nranks)); the
+   ctx's device must be the rank's GPU.  Afterwards sketch_train treats A as the rank's LOCAL shard and
+   all-reduces G on the ctx stream before the top-k solve.  The communicator is destroyed with the ctx;
+   calling tsk_comm_init again replaces it. */
+tsk_status tsk_get_unique_id(unsigned char uid[128]);
+tsk_status tsk_comm_init(tsk_ctx ctx, int nranks, int rank, const unsigned char uid[128]);
 
 /* ---------------------------------------------------------------------- training */
 
@@ -101,9 +116,10 @@ tsk_status sketch_gram(tsk_ctx ctx, const float* A, int64_t D, int m, int n, dou
 tsk_status sketch_topk(tsk_ctx ctx, const double* G64, int m, int k, float* S, double* lambda,
                        const tsk_train_opts* opts, tsk_train_info* info);
 
-/* Algorithm 2 lines 1-2 on one GPU: sketch_gram followed by sketch_topk.  G64_out (optional)
-   receives the Gram.  Multi-GPU: call sketch_gram on each rank's contiguous shard, all-reduce G64
-   (sum), then sketch_topk on every rank (deterministic, identical S everywhere). */
+/* Algorithm 2 lines 1-2: sketch_gram followed by sketch_topk.  G64_out (optional) receives the Gram.
+   Multi-GPU: after tsk_comm_init, A is the rank's local shard and G is all-reduced (NCCL, sum) between
+   the two steps; alternatively call sketch_gram on each shard, all-reduce G64 with the caller's own
+   collective, then sketch_topk on every rank (deterministic, identical S everywhere). */
 tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S, double* lambda,
                         double* G64_out, const tsk_train_opts* opts, tsk_train_info* info);
 

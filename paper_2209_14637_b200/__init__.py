@@ -26,13 +26,14 @@ TSK_OK = 0
 TSK_WARN_RANK_CLAMPED = 1
 TSK_WARN_NOT_CONVERGED = 2
 STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVERGED", -1: "TSK_EINVAL",
-                -2: "TSK_ESHAPE", -3: "TSK_ENOMEM", -4: "TSK_ECUDA", -6: "TSK_EDEVICE", -8: "TSK_ENULL"}
+                -2: "TSK_ESHAPE", -3: "TSK_ENOMEM", -4: "TSK_ECUDA", -5: "TSK_ENCCL", -6: "TSK_EDEVICE",
+                -8: "TSK_ENULL"}
 
 # every symbol include/tsketch.h declares (checked by tests/test_abi.py on CPU)
 EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_status_string", "tsk_launch_count",
             "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2",
             "sketch_train_two_sided", "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe",
-            "tsk_eig_probe", "sketch_train_matrix_free"]
+            "tsk_eig_probe", "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"]
 
 
 class TskError(RuntimeError):
@@ -114,10 +115,12 @@ def lib() -> ctypes.CDLL:
         L.tsk_gram_probe.argtypes = [vp, f32p, i64, i32, i32, f64p, i32, i32, i32]
         L.tsk_eig_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp]
         L.sketch_train_matrix_free.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, vp, vp]
+        L.tsk_get_unique_id.argtypes = [vp]
+        L.tsk_comm_init.argtypes = [vp, i32, i32, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
                   "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2", "sketch_train_two_sided",
                   "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe",
-                  "sketch_train_matrix_free"):
+                  "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -163,6 +166,14 @@ class Context:
     def sync(self):
         _check(lib().tsk_sync(self.handle), "tsk_sync")
 
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """Join the NCCL communicator `uid` (from get_unique_id on one rank, broadcast by the caller) as
+        `rank` of `nranks`; afterwards sketch_train all-reduces the Gram of the local shard."""
+        if len(uid) != 128:
+            raise ValueError("uid must be the 128 bytes of get_unique_id()")
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(lib().tsk_comm_init(self.handle, int(nranks), int(rank), buf), "tsk_comm_init")
+
     @property
     def launches(self) -> int:
         return int(lib().tsk_launch_count(self.handle))
@@ -177,6 +188,13 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id for tsk_comm_init (NCCL loaded at run time; TSK_ENCCL if unavailable)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tsk_get_unique_id(buf), "tsk_get_unique_id")
+    return buf.raw
 
 
 _ctx_cache: dict = {}

@@ -9,6 +9,12 @@
 
 #include "tsk_internal.h"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
 using tsk::Ctx;
 
 namespace {
@@ -99,7 +105,81 @@ static tsk_status stage_slot(tsk_ctx ctx, const void* user, size_t bytes, int sl
   return TSK_OK;
 }
 
+// ---------------------------------------------------------------- NCCL, loaded at run time
+// (types from nccl.h; the library itself is dlopen'ed so libtsketch has no link-time NCCL dependency
+// and shares the copy torch already loaded)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+};
+
+static NcclApi* nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy;
+  });
+  return api.ok ? &api : nullptr;
+}
+
+namespace tsk {
+// G (+)= over all ranks of the ctx's communicator (in place, fp64 sum) on the ctx stream
+tsk_status allreduce_gram(Ctx* c, double* G, size_t n) {
+  if (!c->comm) return TSK_OK;
+  NcclApi* api = nccl_api();
+  if (!api) return TSK_ENCCL;
+  if (api->allReduce(G, G, n, ncclFloat64, ncclSum, reinterpret_cast<ncclComm_t>(c->comm), c->stream) != ncclSuccess)
+    return TSK_ENCCL;
+  return TSK_OK;
+}
+}  // namespace tsk
+
 extern "C" {
+
+tsk_status tsk_get_unique_id(unsigned char uid[128]) {
+  if (!uid) return TSK_ENULL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  NcclApi* api = nccl_api();
+  if (!api) return TSK_ENCCL;
+  ncclUniqueId id;
+  if (api->getUniqueId(&id) != ncclSuccess) return TSK_ENCCL;
+  memcpy(uid, &id, sizeof(id));
+  return TSK_OK;
+}
+
+tsk_status tsk_comm_init(tsk_ctx ctx, int nranks, int rank, const unsigned char uid[128]) {
+  if (!ctx || !uid) return TSK_ENULL;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return TSK_EINVAL;
+  NcclApi* api = nccl_api();
+  if (!api) return TSK_ENCCL;
+  Ctx& c = ctx->c;
+  cudaSetDevice(c.device);
+  if (c.comm) {
+    cudaStreamSynchronize(c.stream);
+    api->commDestroy(reinterpret_cast<ncclComm_t>(c.comm));
+    c.comm = nullptr;
+  }
+  ncclUniqueId id;
+  memcpy(&id, uid, sizeof(id));
+  ncclComm_t comm = nullptr;
+  if (api->commInitRank(&comm, nranks, id, rank) != ncclSuccess) return TSK_ENCCL;
+  c.comm = comm;
+  c.nranks = nranks;
+  c.rank = rank;
+  return TSK_OK;
+}
 
 const char* tsk_status_string(tsk_status s) {
   switch (s) {
@@ -110,6 +190,7 @@ const char* tsk_status_string(tsk_status s) {
     case TSK_ESHAPE: return "unsupported shape / alignment (n % 4 != 0 or misaligned pointer)";
     case TSK_ENOMEM: return "device allocation failed";
     case TSK_ECUDA: return "CUDA error";
+    case TSK_ENCCL: return "NCCL unavailable or NCCL call failed";
     case TSK_EDEVICE: return "device is not sm_100 (B200)";
     case TSK_ENULL: return "required pointer is NULL";
   }
@@ -145,6 +226,10 @@ tsk_status tsk_destroy(tsk_ctx ctx) {
   for (int i = 0; i < tsk::WS_COUNT; ++i)
     if (c.ws[i]) cudaFree(c.ws[i]);
   if (c.host_pinned) cudaFreeHost(c.host_pinned);
+  if (c.comm) {
+    if (NcclApi* api = nccl_api()) api->commDestroy(reinterpret_cast<ncclComm_t>(c.comm));
+    c.comm = nullptr;
+  }
   if (c.side) cudaStreamDestroy(c.side);
   for (auto& ev : c.ev)
     if (ev) cudaEventDestroy(ev);
@@ -334,6 +419,7 @@ tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, in
   else
     s = gram_host(ctx, A, D, m, n, G, nullptr, 0, opts, info);
   if (is_error(s)) return s;
+  if (is_error(s = tsk::allreduce_gram(c, G, (size_t)m * m))) return s;  // multi-GPU (tsk_comm_init)
   DevBuf sb, lb;
   if (is_error(s = stage_slot(ctx, S, (size_t)k * m * 4, 2, sb, false))) return s;
   if (lambda && is_error(s = stage_slot(ctx, lambda, (size_t)k * 8, 3, lb, false))) return s;

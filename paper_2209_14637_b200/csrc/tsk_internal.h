@@ -115,6 +115,9 @@ struct Ctx {
     return host_pinned;
   }
   void count_launch(int n = 1) { launches += n; }
+  // NCCL communicator of tsk_comm_init (ncclComm_t, opaque here; nullptr = single GPU)
+  void* comm = nullptr;
+  int nranks = 1, rank = 0;
   // side stream + fork/join events (batched SCW runs two halves of a chunk concurrently), created on
   // first use and destroyed with the ctx
   cudaStream_t side = nullptr;

@@ -29,6 +29,22 @@ def reduce_gram(G64: torch.Tensor, group=None) -> torch.Tensor:
     return G64
 
 
+def init_native_comm(ctx=None, group=None):
+    """Give the library its own NCCL communicator over the ranks of `group` (tsk_comm_init): rank 0
+    draws the unique id, torch.distributed broadcasts it.  Afterwards ``sketch_train`` all-reduces the
+    Gram of the local shard itself (C ABI path); ``train`` below keeps torch's all-reduce."""
+    from . import context, get_unique_id
+
+    ctx = ctx or context()
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    obj = [get_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.comm_init(world, rank, obj[0])
+    return ctx
+
+
 def train(A_local: torch.Tensor, k: int, group=None, opts=None, G64: Optional[torch.Tensor] = None):
     """Algorithm 2 lines 1-2 over all ranks of `group`: local Gram of this rank's shard,
     all-reduce, top-k eigenvectors.  Returns (S [k, m], lambda [k], info, status)."""

@@ -306,3 +306,22 @@ def test_virtual_shards_match_single_gram(world):
     e1 = tucker1.kyfan_energy(Go, S1.cpu().double().numpy())
     es = tucker1.kyfan_energy(Go, Ss.cpu().double().numpy())
     assert abs(e1 - es) <= 1e-7 * e1
+
+
+def test_native_nccl_communicator_single_rank():
+    """tsk_get_unique_id / tsk_comm_init: with the library's own NCCL communicator,
+    sketch_train all-reduces the local Gram (one rank here: the pool gives one GPU) and returns the
+    same sketch, bit for bit, as without it."""
+    c = datagen.CONFIGS["C2"]
+    A = datagen.generate(c, "train", 0, 60).cuda()
+    S0, lam0, _, _ = tsk.sketch_train(A, c.k)
+    uid = tsk.get_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
+    ctx = tsk.Context(0)
+    ctx.comm_init(1, 0, uid)
+    S1, lam1, _, _ = tsk.sketch_train(A, c.k, ctx=ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(S0, S1) and torch.equal(lam0, lam1)
+    with pytest.raises(tsk.TskError):
+        ctx.comm_init(2, 2, uid)  # rank outside [0, nranks)
+    ctx.close()
