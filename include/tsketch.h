@@ -51,6 +51,7 @@ typedef enum {
   TSK_ECUDA = -4,             /* CUDA runtime / launch / device fault */
   TSK_ENCCL = -5,             /* NCCL library not loadable, or an NCCL call failed */
   TSK_EDEVICE = -6,           /* device is not compute capability 10.0 (sm_100a) */
+  TSK_ENONFINITE = -7,        /* NaN/Inf in the training input, only with opts->check_finite */
   TSK_ENULL = -8              /* a required pointer is NULL */
 } tsk_status;
 
@@ -92,6 +93,10 @@ typedef struct {
   const float* init_S; /* optional DEVICE [k][m] warm start of the subspace iteration (e.g. the sketch of
                           the stream so far); NULL = deterministic pseudo-random start.
                           Only the starting block changes: S is still the top-k of G to tol. */
+  int check_finite;    /* != 0 (sketch_gram / sketch_train): scan the training input first (one HBM pass)
+                          and return TSK_ENONFINITE if any entry is NaN or Inf (matrices are
+                          finite); device inputs: nothing is computed; host inputs are checked per staged
+                          chunk, so G64 is unspecified after the error */
 } tsk_train_opts;
 
 typedef struct {

@@ -26,7 +26,7 @@ TSK_OK = 0
 TSK_WARN_RANK_CLAMPED = 1
 TSK_WARN_NOT_CONVERGED = 2
 STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVERGED", -1: "TSK_EINVAL",
-                -2: "TSK_ESHAPE", -3: "TSK_ENOMEM", -4: "TSK_ECUDA", -5: "TSK_ENCCL", -6: "TSK_EDEVICE",
+                -2: "TSK_ESHAPE", -3: "TSK_ENOMEM", -4: "TSK_ECUDA", -5: "TSK_ENCCL", -6: "TSK_EDEVICE", -7: "TSK_ENONFINITE",
                 -8: "TSK_ENULL"}
 
 # every symbol include/tsketch.h declares (checked by tests/test_abi.py on CPU)
@@ -45,7 +45,7 @@ class TskError(RuntimeError):
 class TrainOpts(ctypes.Structure):
     _fields_ = [("oversample", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
                 ("dense_max_m", ctypes.c_int), ("gemm_chain", ctypes.c_int), ("gemm_splits", ctypes.c_int),
-                ("init_S", ctypes.c_void_p)]
+                ("init_S", ctypes.c_void_p), ("check_finite", ctypes.c_int)]
 
 
 class TrainInfo(ctypes.Structure):

@@ -191,6 +191,7 @@ const char* tsk_status_string(tsk_status s) {
     case TSK_ENOMEM: return "device allocation failed";
     case TSK_ECUDA: return "CUDA error";
     case TSK_ENCCL: return "NCCL unavailable or NCCL call failed";
+    case TSK_ENONFINITE: return "non-finite (NaN/Inf) entry in the training input";
     case TSK_EDEVICE: return "device is not sm_100 (B200)";
     case TSK_ENULL: return "required pointer is NULL";
   }
@@ -260,8 +261,36 @@ tsk_status tsk_sync(tsk_ctx ctx) {
 int64_t tsk_launch_count(tsk_ctx ctx) { return ctx ? ctx->c.launches : -1; }
 
 // ------------------------------------------------------------------------------ training
+// any NaN / Inf among n4 float4 (exponent field all ones); the order of the flag updates is irrelevant
+__global__ void nonfinite_kernel(const float4* __restrict__ x, long long n4, int* __restrict__ flag) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = x[i];
+    bad |= ((__float_as_uint(v.x) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(v.y) & 0x7F800000u) == 0x7F800000u) |
+           ((__float_as_uint(v.z) & 0x7F800000u) == 0x7F800000u) | ((__float_as_uint(v.w) & 0x7F800000u) == 0x7F800000u);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+static tsk_status check_finite(Ctx* c, const float* A, long long count) {
+  int* flag = reinterpret_cast<int*>(c->workspace(tsk::WS_CHECK, 64));
+  int* hflag = reinterpret_cast<int*>(c->pinned(64));
+  if (!flag || !hflag) return TSK_ENOMEM;
+  if (cudaMemsetAsync(flag, 0, sizeof(int), c->stream) != cudaSuccess) return TSK_ECUDA;
+  nonfinite_kernel<<<4 * c->num_sms, 256, 0, c->stream>>>(reinterpret_cast<const float4*>(A), count / 4, flag);
+  c->count_launch();
+  if (cudaMemcpyAsync(hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return TSK_ECUDA;
+  return *hflag ? TSK_ENONFINITE : TSK_OK;
+}
+
 static tsk_status gram_device(Ctx* c, const float* A, int64_t D, int m, int n, double* G64, float* G32,
                               int accumulate, const tsk_train_opts* opts, tsk_train_info* info) {
+  if (opts && opts->check_finite) {
+    const tsk_status fs = check_finite(c, A, (long long)D * m * n);  // n % 4 == 0: whole float4s
+    if (fs != TSK_OK) return fs;
+  }
   tsk::GemmProblem p;
   p.X = A;
   p.Y = A;

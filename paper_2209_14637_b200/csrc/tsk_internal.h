@@ -64,6 +64,7 @@ enum WorkspaceId {
   WS_MF_Q32,       // matrix-free sketch: K^T (fp32, tensor-core operand)
   WS_MF_SMALL,     // matrix-free sketch: small fp64 matrices, flags
   WS_MF_SCR,       // matrix-free sketch: fp64 GEMM split scratch
+  WS_CHECK,        // input validation flag (check_finite)
   WS_COUNT
 };
 

@@ -55,7 +55,7 @@ def test_library_is_sm100a_tcgen05(lib):
 
 def test_status_strings(lib):
     lib.tsk_status_string.restype = ctypes.c_char_p
-    for s in (0, 1, 2, -1, -2, -3, -4, -5, -6, -8):
+    for s in (0, 1, 2, -1, -2, -3, -4, -5, -6, -7, -8):
         assert lib.tsk_status_string(s)
     assert b"unknown" in lib.tsk_status_string(12345)
 

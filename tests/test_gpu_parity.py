@@ -325,3 +325,19 @@ def test_native_nccl_communicator_single_rank():
     with pytest.raises(tsk.TskError):
         ctx.comm_init(2, 2, uid)  # rank outside [0, nranks)
     ctx.close()
+
+
+def test_check_finite_rejects_nan_and_inf():
+    """opts.check_finite (SURVEY §8(b) TSK_ENONFINITE): a NaN or an Inf anywhere in the training
+    stack is reported before any Gram work; finite input passes unchanged."""
+    c = datagen.CONFIGS["C2"]
+    A = datagen.generate(c, "train", 0, 20).cuda()
+    G_ok, _ = tsk.sketch_gram(A, opts={"check_finite": 1})
+    G_ref, _ = tsk.sketch_gram(A)
+    assert torch.equal(G_ok, G_ref)
+    for bad in (float("nan"), float("inf"), -float("inf")):
+        B = A.clone()
+        B[13, 200, 255] = bad
+        with pytest.raises(tsk.TskError) as e:
+            tsk.sketch_train(B, c.k, opts={"check_finite": 1})
+        assert e.value.status == -7
