@@ -97,6 +97,8 @@ typedef struct {
                           and return TSK_ENONFINITE if any entry is NaN or Inf (matrices are
                           finite); device inputs: nothing is computed; host inputs are checked per staged
                           chunk, so G64 is unspecified after the error */
+  int cheb_degree;     /* cap on the Chebyshev filter degree per outer iteration (0 = adaptive, <= 12: the
+                          largest degree whose dynamic range T_d(x_max) stays <= 1e6) */
 } tsk_train_opts;
 
 typedef struct {
@@ -105,6 +107,8 @@ typedef struct {
   double max_resid;   /* max_{i<k} ||G s_i - theta_i s_i|| / theta_1 */
   int gram_splits;    /* K splits used by the Gram kernel */
   int gram_tiles;     /* 128x128 output tiles computed (lower triangle) */
+  double gap_est;     /* theta_k / theta_{k+1} from the last Rayleigh-Ritz step (the eigengap of reading c6;
+                         +inf when the block holds no (k+1)-th value or it is 0) */
 } tsk_train_info;
 
 /* Mode-1 Gram of a stack of D training matrices:

@@ -45,12 +45,12 @@ class TskError(RuntimeError):
 class TrainOpts(ctypes.Structure):
     _fields_ = [("oversample", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
                 ("dense_max_m", ctypes.c_int), ("gemm_chain", ctypes.c_int), ("gemm_splits", ctypes.c_int),
-                ("init_S", ctypes.c_void_p), ("check_finite", ctypes.c_int)]
+                ("init_S", ctypes.c_void_p), ("check_finite", ctypes.c_int), ("cheb_degree", ctypes.c_int)]
 
 
 class TrainInfo(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int), ("kyfan", ctypes.c_double), ("max_resid", ctypes.c_double),
-                ("gram_splits", ctypes.c_int), ("gram_tiles", ctypes.c_int)]
+                ("gram_splits", ctypes.c_int), ("gram_tiles", ctypes.c_int), ("gap_est", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

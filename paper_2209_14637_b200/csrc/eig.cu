@@ -305,6 +305,9 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       for (double v : h) kf += v;
       info->kyfan = kf;
       info->max_resid = 0.0;
+      double lk1 = 0.0;
+      if (k < m) cudaMemcpy(&lk1, lam + k, 8, cudaMemcpyDeviceToHost);
+      info->gap_est = lk1 > 0.0 ? h[k - 1] / lk1 : INFINITY;
     }
     return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
   }
@@ -496,7 +499,7 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     if (b > 0.0 && xmax > 1.0 + 1e-12) {
       const double ach = acosh(xmax);
       d = (int)std::floor(std::log(2e6) / ach);  // T_d(x) ~ exp(d acosh x) / 2 <= 1e6
-      d = std::max(1, std::min(d, 12));
+      d = std::max(1, std::min(d, opt.cheb_degree > 0 ? std::min(12, opt.cheb_degree) : 12));
     }
     if (getenv("TSK_EIG_TRACE")) fprintf(stderr, "[eig]   lock %d, filter degree %d on [0, %.4e], x_max %.3e\n", nnew, d, b, xmax);
     copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(X, pa, off, Y0, pn, 0, m, pn);
@@ -568,6 +571,8 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     for (double v : hl) kyfan += v;
     info->kyfan = kyfan;
     info->max_resid = max_res;
+    // hostbuf holds the Ritz values of the last Rayleigh-Ritz step (active block, decreasing)
+    info->gap_est = (kr >= 1 && kr < pa && hostbuf[kr] > 0.0) ? hostbuf[kr - 1] / hostbuf[kr] : INFINITY;
   }
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   return converged ? TSK_OK : TSK_WARN_NOT_CONVERGED;
