@@ -53,6 +53,51 @@ def workload_desc(c, n_gpus):
             "l2_policy": f"inputs larger than L2 ({c.train_bytes / 1e9:.1f} GB training stream per step)"}
 
 
+class NvmlClockSampler:
+    """SM clocks and throttle reasons sampled every 5 ms through NVML (nvidia_ml_py) in a background
+    thread during the timed region; ClockSampler (nvidia-smi -lms) is the fallback."""
+
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+
+    def __init__(self, index):
+        import threading
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.rows = []
+        self.stop_flag = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_flag.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), get_reasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def stop(self):
+        self.stop_flag.set()
+        self.t.join()
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({nm for _, bits in self.rows for nm, b in self.REASONS.items() if bits & b})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml"}
+
+
+def clock_sampler(index):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -217,7 +262,7 @@ def run_tsketch(args, c):
         step(False)
     barrier(world)
     l0 = ctx.launches
-    clocks = ClockSampler(local) if rank == 0 else None
+    clocks = clock_sampler(local) if rank == 0 else None
     barrier(world)
     e_start = torch.cuda.Event(enable_timing=True)
     e_end = torch.cuda.Event(enable_timing=True)
