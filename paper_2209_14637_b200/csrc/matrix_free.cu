@@ -234,6 +234,9 @@ tsk_status matrix_free_sketch(Ctx* ctx, const float* A, long long D, int m, int 
   if ((st = mf_rr_gram(ctx, Z, D, n, wz, H)) != TSK_OK) return st;
   // top-k eigenpairs of H: the eigensolver of sketch_topk with fp64 products (w <= 256)
   tsk_train_opts eo{};
+  // H carries the 3xTF32 error of the Z_d products (~1e-6 relative, tests): a Ritz residual of 1e-9 theta_1
+  // is far below it (the eigensolver's fp64 default, 1e-11, took twice the iterations)
+  eo.tol = 1e-9;
   tsk_train_info ei{};
   float* Sh = reinterpret_cast<float*>(W + (size_t)wz * k);  // [k][wz] fp32 (unused output)
   if ((st = topk_eigen_ex(ctx, H, wz, k, Sh, lam, &eo, &ei, 1, W)) < 0) return st;
