@@ -99,12 +99,16 @@ typedef struct {
                           chunk, so G64 is unspecified after the error */
   int cheb_degree;     /* cap on the Chebyshev filter degree per outer iteration (0 = adaptive, <= 12: the
                           largest degree whose dynamic range T_d(x_max) stays <= 1e6) */
+  int tol_active;      /* != 0: once dominant pairs are locked, Ritz residuals are measured against the top
+                          of the remaining (deflated) spectrum instead of theta_1 -- tighter eigenvectors
+                          below a dominant eigenvalue (e.g. a frame mean), more iterations; max_resid is
+                          then reported on that scale */
 } tsk_train_opts;
 
 typedef struct {
   int iters;          /* subspace iterations run (0 for the dense path) */
   double kyfan;       /* sum_{i<k} theta_i, the Ky Fan energy tr(S G S^T) */
-  double max_resid;   /* max_{i<k} ||G s_i - theta_i s_i|| / theta_1 */
+  double max_resid;   /* max_{i<k} ||G s_i - theta_i s_i|| / theta_1 (/ the active top with tol_active) */
   int gram_splits;    /* K splits used by the Gram kernel */
   int gram_tiles;     /* 128x128 output tiles computed (lower triangle) */
   double gap_est;     /* theta_k / theta_{k+1} from the last Rayleigh-Ritz step (the eigengap of reading c6;

@@ -45,7 +45,8 @@ class TskError(RuntimeError):
 class TrainOpts(ctypes.Structure):
     _fields_ = [("oversample", ctypes.c_int), ("max_iters", ctypes.c_int), ("tol", ctypes.c_double),
                 ("dense_max_m", ctypes.c_int), ("gemm_chain", ctypes.c_int), ("gemm_splits", ctypes.c_int),
-                ("init_S", ctypes.c_void_p), ("check_finite", ctypes.c_int), ("cheb_degree", ctypes.c_int)]
+                ("init_S", ctypes.c_void_p), ("check_finite", ctypes.c_int), ("cheb_degree", ctypes.c_int),
+                ("tol_active", ctypes.c_int)]
 
 
 class TrainInfo(ctypes.Structure):

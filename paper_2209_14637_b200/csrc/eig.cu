@@ -436,21 +436,30 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     const double* hres = hostbuf + p;
     const int* hflags = reinterpret_cast<const int*>(hostbuf + 2 * p);
     if (nl == 0) theta_top = hth[0];
-    max_res = 0.0;
-    for (int c = 0; c < kr; ++c) max_res = std::max(max_res, hres[c]);
-    max_res /= theta_top > 0 ? theta_top : 1.0;
-    const double floor_rel = f64 ? 1e-14 : 4e-8;  // working-precision floor of the G Q products
-    const double tol_eff = std::max(tol, theta_top > 0 ? floor_rel * gfro / theta_top : tol);
-    double kf_now = 0.0;  // Ky Fan energy of the current k wanted values (locked + active)
+    double kf_now = 0.0;    // Ky Fan energy of the current k wanted values (locked + active)
+    double locked2 = 0.0;   // sum of the squared locked Ritz values
     {
       std::vector<double> hl(nl);
       if (nl > 0) {
         cudaMemcpyAsync(hl.data(), thl, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
       }
-      for (double v : hl) kf_now += v;
+      for (double v : hl) {
+        kf_now += v;
+        locked2 += v * v;
+      }
       for (int c = 0; c < kr; ++c) kf_now += hth[c];
     }
+    // residual scale: theta_1 (reading c15), or with tol_active the top of the active (deflated)
+    // block, whose Gram norm ||G'||_F ~ sqrt(||G||_F^2 - sum locked theta^2) also sets the floor
+    const bool act = opt.tol_active && nl > 0 && hth[0] > 0.0;
+    const double ref = act ? hth[0] : theta_top;
+    const double gref = act ? std::sqrt(std::max(gfro2 - locked2, 0.0)) : gfro;
+    max_res = 0.0;
+    for (int c = 0; c < kr; ++c) max_res = std::max(max_res, hres[c]);
+    max_res /= ref > 0 ? ref : 1.0;
+    const double floor_rel = f64 ? 1e-14 : 4e-8;  // working-precision floor of the G Q products
+    const double tol_eff = std::max(tol, ref > 0 ? floor_rel * gref / ref : tol);
     if (kyfan_prev > 0 && std::fabs(kf_now - kyfan_prev) <= 1e-12 * kf_now) ++kyfan_still;
     else kyfan_still = 0;
     kyfan_prev = kf_now;
@@ -474,7 +483,7 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     if (outer == max_iters) break;
     // ---- lock the leading converged pairs well above the wanted edge (theta >= 2 theta_{k-1})
     int nnew = 0;
-    while (nnew < kr - 1 && hres[nnew] <= tol * theta_top && hth[nnew] >= 2.0 * hth[kr - 1]) ++nnew;
+    while (nnew < kr - 1 && hres[nnew] <= tol * ref && hth[nnew] >= 2.0 * hth[kr - 1]) ++nnew;
     const double* tha = theta;  // device Ritz values of the active block
     int off = 0;                // first active column of X / theta after locking
     if (nnew > 0) {

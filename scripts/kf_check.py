@@ -6,7 +6,12 @@ from oracle import tucker1
 c = datagen.CONFIGS["C4"]
 A = datagen.generate(c, "train", device="cuda")
 G = torch.empty(c.m, c.m, dtype=torch.float64, device="cuda")
-S, lam, info, st = tsk.sketch_train(A, c.k, G64_out=G)
+opts = {"tol_active": 1} if "--active" in sys.argv else None
+S, lam, info, st = tsk.sketch_train(A, c.k, opts=opts, G64_out=G)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); S, lam, info, st = tsk.sketch_topk(G, c.k, opts=opts); e1.record(); torch.cuda.synchronize()
+print("topk ms", e0.elapsed_time(e1), "products", info.iters, "status", st)
 Gg = G.cpu().numpy(); w = np.sort(np.linalg.eigvalsh(Gg))[::-1]
 Sd = S.cpu().double().numpy()
 kf = tucker1.kyfan_energy(Gg, Sd)

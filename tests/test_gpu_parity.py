@@ -347,3 +347,25 @@ def test_check_finite_rejects_nan_and_inf():
         with pytest.raises(tsk.TskError) as e:
             tsk.sketch_train(B, c.k, opts={"check_finite": 1})
         assert e.value.status == -7
+
+
+def test_tol_active_tightens_the_non_dominant_subspace():
+    """opts.tol_active: with the frame mean (C4's dominant eigenvalue, ~1e4 x the rest) locked, residuals
+    are measured against the top of the deflated spectrum, so the energy the sketch captures OUTSIDE the
+    dominant direction reaches the optimum too (default stopping rule, reading c15: ~1e-5 short)."""
+    c = datagen.CONFIGS["C4"]
+    A = datagen.generate(c, "train", 0, 300, device="cuda")
+    G, _ = tsk.sketch_gram(A)
+    Gg = G.cpu().numpy()
+    w = np.sort(np.linalg.eigvalsh(Gg))[::-1]
+
+    def non_dominant_deficit(S):
+        Sd = S.cpu().double().numpy()
+        kf = tucker1.kyfan_energy(Gg, Sd)
+        return (w[1:c.k].sum() - (kf - w[0])) / w[1:c.k].sum()
+
+    S0, _, _, st0 = tsk.sketch_topk(G, c.k)
+    S1, _, info1, st1 = tsk.sketch_topk(G, c.k, opts={"tol_active": 1})
+    assert st0 == 0 and st1 == 0
+    d0, d1 = non_dominant_deficit(S0), non_dominant_deficit(S1)
+    assert d1 <= 1e-6 and d1 <= d0, (d0, d1)
