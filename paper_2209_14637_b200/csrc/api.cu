@@ -231,7 +231,8 @@ tsk_status tsk_destroy(tsk_ctx ctx) {
     if (NcclApi* api = nccl_api()) api->commDestroy(reinterpret_cast<ncclComm_t>(c.comm));
     c.comm = nullptr;
   }
-  if (c.side) cudaStreamDestroy(c.side);
+  for (auto& st : c.side)
+    if (st) cudaStreamDestroy(st);
   for (auto& ev : c.ev)
     if (ev) cudaEventDestroy(ev);
   CtxExt* e = ext_of(ctx);

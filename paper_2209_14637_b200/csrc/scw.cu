@@ -508,21 +508,25 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     if ((st = launch_status("scw")) != TSK_OK) return st;
     return TSK_OK;
   };
+  const int nparts_max = getenv("TSK_SCW_PARTS") ? std::max(1, std::min(Ctx::kSide + 1, atoi(getenv("TSK_SCW_PARTS")))) : 2;
   for (long long b0 = 0; b0 < B; b0 += chunk) {
     const int bc = (int)std::min(chunk, B - b0);
-    tsk_status st;
-    if (two && bc >= 64) {
-      const int h0 = bc / 2;
-      cudaEventRecord(ctx->ev[0], s0);  // fork: the side stream starts after the work before this call
-      cudaStreamWaitEvent(ctx->side, ctx->ev[0], 0);
-      st = half(b0, h0, 0, s0, ctx->ev[1]);
-      if (st == TSK_OK) {
-        cudaStreamWaitEvent(ctx->side, ctx->ev[1], 0);
-        st = half(b0 + h0, bc - h0, h0, ctx->side, nullptr);
+    tsk_status st = TSK_OK;
+    const int parts = two ? std::min(nparts_max, bc / 32) : 1;
+    if (parts >= 2) {
+      cudaEventRecord(ctx->ev[0], s0);  // fork: the side streams start after the work before this call
+      for (int j = 1; j < parts; ++j) cudaStreamWaitEvent(ctx->side[j - 1], ctx->ev[0], 0);
+      for (int j = 0; j < parts && st == TSK_OK; ++j) {
+        const int o0 = (int)((long long)bc * j / parts), o1 = (int)((long long)bc * (j + 1) / parts);
+        cudaStream_t sj = j == 0 ? s0 : ctx->side[j - 1];
+        if (j > 0) cudaStreamWaitEvent(sj, ctx->ev[j], 0);  // one phase behind part j - 1
+        st = half(b0 + o0, o1 - o0, o0, sj, j + 1 < parts ? ctx->ev[j + 1] : nullptr);
       }
       ctx->stream = s0;
-      cudaEventRecord(ctx->ev[2], ctx->side);  // join
-      cudaStreamWaitEvent(s0, ctx->ev[2], 0);
+      for (int j = 1; j < parts; ++j) {  // join
+        cudaEventRecord(ctx->ev[Ctx::kSide + j], ctx->side[j - 1]);
+        cudaStreamWaitEvent(s0, ctx->ev[Ctx::kSide + j], 0);
+      }
     } else {
       st = half(b0, bc, 0, s0, nullptr);
       ctx->stream = s0;

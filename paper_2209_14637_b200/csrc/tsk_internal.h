@@ -121,15 +121,16 @@ struct Ctx {
   int nranks = 1, rank = 0;
   // side stream + fork/join events (batched SCW runs two halves of a chunk concurrently), created on
   // first use and destroyed with the ctx
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  static constexpr int kSide = 3;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t ev[2 * kSide + 1] = {};  // [0] fork, [1 + j] after part j's first product, [1 + kSide + j] join
   bool side_ready() {
-    if (side) return true;
-    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) {
-      side = nullptr;
-      cudaGetLastError();
-      return false;
-    }
+    if (side[0]) return true;
+    for (auto& st : side)
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
     for (auto& e : ev)
       if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
