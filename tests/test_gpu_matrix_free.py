@@ -146,3 +146,18 @@ def test_matrix_free_c4_scale():
     te0, _ = oscw.test_error(e0, eopt)
     te1, _ = oscw.test_error(e1, eopt)
     assert te1 <= te0 * 1.5 + 1e-3, (te0, te1)
+
+
+def test_matrix_free_degenerate_sizes():
+    """k = 1 and a single training matrix (D = 1): the block Krylov sketch of one frame is the top
+    left singular vector of that frame (the oracle, same start block); p = m (q = 0) is exact."""
+    g = torch.Generator().manual_seed(11)
+    A = torch.rand(1, 40, 24, generator=g)
+    S, lam, info, st, So, th, K = _run(A, 1, 3, 3)
+    assert st == 0 and info["width"] == 16
+    assert abs(lam[0] - th[0]) <= 1e-5 * th[0]
+    U, s, _ = np.linalg.svd(A[0].double().numpy())
+    assert abs(abs(float(S[0] @ U[:, 0])) - 1.0) <= 1e-6
+    np.testing.assert_allclose(lam[0], s[0] ** 2, rtol=1e-5)
+    S, lam, info, st, So, th, K = _run(A, 2, 38, 0)   # p = m = 40: exact top-2
+    np.testing.assert_allclose(lam, s[:2] ** 2, rtol=1e-5)
