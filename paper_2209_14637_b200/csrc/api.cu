@@ -2,18 +2,15 @@
 // pointer handling, and composition of the kernels into the calls of Algorithm 2
 // (PAPER.md:156-169).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL itself is dlopen'ed (nccl_api below)
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <new>
 
 #include "tsk_internal.h"
-
-#include <dlfcn.h>
-#include <nccl.h>
-
-#include <cstring>
-#include <mutex>
 
 using tsk::Ctx;
 
