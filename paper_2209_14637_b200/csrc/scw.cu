@@ -403,6 +403,18 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   double* mu_all = small + 4 * chunk * kk;
   double* sig2_all = mu_all + chunk * k;
   scw_attrs();
+  // S is the broadcast TMA operand of the SA product: its row pitch must be a multiple of 16 bytes, so
+  // for m % 4 != 0 it is copied once into a padded buffer (the tensor map's extent stays m: the pad is
+  // never read)
+  const int ms = (m + 3) & ~3;
+  if (ms != m) {
+    float* Sp = reinterpret_cast<float*>(ctx->workspace(WS_SCW_S, (size_t)k * ms * 4));
+    if (!Sp) return TSK_ENOMEM;
+    if (cudaMemcpy2DAsync(Sp, (size_t)ms * 4, S, (size_t)m * 4, (size_t)m * 4, k, cudaMemcpyDeviceToDevice,
+                          s0) != cudaSuccess)
+      return TSK_ECUDA;
+    S = Sp;
+  }
   // Each chunk runs as two halves on two streams, the second started one phase (its SA product)
   // behind the first, so the latency-bound small solves of one half (row Grams, pivoted Cholesky,
   // batched Jacobi, factor combinations) overlap the HBM/tensor-bound products of the other.
@@ -436,8 +448,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       gp.x_row_stride = n;
       gp.x_slice_stride = (long long)m * n;
       gp.ybc = 1;
-      gp.y_row_stride = m;
-      gp.y_slice_stride = m;
+      gp.y_row_stride = ms;
+      gp.y_slice_stride = ms;
       gp.batch = 1;
       gp.bn = k <= 64 ? 64 : 128;
       gp.dout = Bm;

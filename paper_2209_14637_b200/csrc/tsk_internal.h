@@ -46,6 +46,7 @@ enum WorkspaceId {
   WS_SCW_3,
   WS_SCW_4,
   WS_SCW_5,
+  WS_SCW_S,        // SCW: S with a 16-byte row pitch when m % 4 != 0
   WS_GRAM,       // fp64 Gram for sketch_train
   WS_JACOBI,
   WS_GEMM_PROGRESS,

@@ -276,6 +276,17 @@ def test_scw_edge_cases():
     np.testing.assert_array_equal(e_h, tsk.scw_error(T.cuda(), S, c.r).cpu().numpy())
 
 
+@pytest.mark.parametrize("m,n,k,r", [(70, 36, 9, 4), (133, 200, 17, 17), (1, 8, 1, 1), (257, 4, 3, 2)])
+def test_scw_ragged_rows(m, n, k, r):
+    """m % 4 != 0 (S is re-pitched for the TMA), n = 4, m = 1, r = k: SCW errors against the oracle
+    (found by scripts/random_sweep.py: m % 4 != 0 used to return TSK_ESHAPE)."""
+    g = torch.Generator().manual_seed(m * 7 + n)
+    A = torch.rand(12, m, n, generator=g) - 0.3
+    T = torch.rand(5, m, n, generator=g) - 0.3
+    S, lam, info, st = tsk.sketch_train(A.cuda(), k)
+    _scw_parity(T, S, r)
+
+
 def test_theorem1_holds_for_gpu_outputs():
     """P8 on the whole GPU path: GPU S, GPU SCW errors on the training set."""
     c = datagen.CONFIGS["C2"]
