@@ -9,14 +9,16 @@ from oracle import scw as oscw, tucker1  # noqa: E402
 
 ncase = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+big = "--big" in sys.argv  # m up to 1500 (subspace-iteration eigensolver), k up to 100
 bad = 0
 for t in range(ncase):
-    m = int(rng.integers(2, 700)); n = int(rng.integers(1, 200)) * 4; D = int(rng.integers(1, 12))
+    m = int(rng.integers(257, 1500)) if big else int(rng.integers(2, 700))
+    n = int(rng.integers(1, 200)) * 4; D = int(rng.integers(1, 12))
     A = torch.from_numpy(rng.random((D, m, n), dtype=np.float32) - 0.3)
     G, _ = tsk.sketch_gram(A.cuda())
     Go = tucker1.mode1_gram(A.numpy())
     ge = float(np.linalg.norm(G.cpu().numpy() - Go) / np.linalg.norm(Go))
-    k = int(rng.integers(1, min(m, 60) + 1)); r = int(rng.integers(1, min(k, n, m) + 1))
+    k = int(rng.integers(1, min(m, 100 if big else 60) + 1)); r = int(rng.integers(1, min(k, n, m, 64) + 1))
     S, lam, info, st = tsk.sketch_topk(G, k)
     Sd = S.cpu().double().numpy()
     w = np.sort(np.linalg.eigvalsh(Go))[::-1]
