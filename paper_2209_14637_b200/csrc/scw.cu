@@ -567,7 +567,10 @@ tsk_status scw2_run(Ctx* ctx, const float* A, long long B, int m, int n, const f
   float* Zt = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
   float* Yt = reinterpret_cast<float*>(ctx->workspace(WS_SCW2_0, chunk * lm * 4));
   float* Pt = reinterpret_cast<float*>(ctx->workspace(WS_SCW2_1, chunk * lm * 4));
-  const size_t nsmall = chunk * (2 * kk + 2 * ll + 2 * (size_t)l * k + (size_t)l * r + kk + 2 * (size_t)k + 2 * (size_t)l);
+  // per matrix: Cq, Wq, H2, W2 [k][k]; Cp, Wp [l][l]; Mx [l][k]; CL [l][r]; muq, sig2 [k]; mup [l]
+  // (the sum was short by k(k - l) - l doubles per matrix: for k > l + 1 the last arrays of a chunk
+  // ran past the allocation -- found by scripts/random_sweep2.py)
+  const size_t nsmall = chunk * (4 * kk + 2 * ll + (size_t)l * k + (size_t)l * r + 2 * (size_t)k + (size_t)l);
   double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW2_2, nsmall * 8));
   const int tiles = (int)(nb(n, 128) * nb(m, 128)) * 8;
   const int ldf = (L || R) ? r : (r + 3) & ~3;

@@ -142,3 +142,19 @@ def test_two_sided_scw_special_cases():
     Ah = (L[0].double() @ R[0].double().T).cpu().numpy()
     Aho = tucker2.two_sided_scw(T[0].numpy(), S.double().numpy(), orth_rows(12, n, 4).double().numpy(), r)
     assert relF(Ah, Aho) <= 1e-5
+
+
+@pytest.mark.parametrize("m,n,k,l,r", [(188, 204, 18, 6, 5), (96, 40, 30, 4, 3)])
+def test_two_sided_scw_k_much_larger_than_l_fresh_context(m, n, k, l, r):
+    """k >> l on a FRESH context (workspaces sized by this call alone): the small-matrix workspace of the
+    two-sided SCW used to be short by k(k - l) - l doubles per matrix, corrupting the later matrices of
+    a batch (found by scripts/random_sweep2.py)."""
+    rng = np.random.default_rng(m + k)
+    T = torch.from_numpy(rng.random((3, m, n), dtype=np.float32) - 0.3)
+    S = torch.tensor(orth_rows(k, m, 1).numpy())
+    W = torch.tensor(orth_rows(l, n, 2).numpy())
+    ctx = tsk.Context(0)
+    e = tsk.two_sided_scw_error(T.cuda(), S.cuda(), W.cuda(), r, ctx=ctx).cpu().numpy()
+    ctx.close()
+    eo = tucker2.two_sided_scw_errors(T.numpy(), S.double().numpy(), W.double().numpy(), r)
+    assert np.all(np.abs(e - eo) <= 1e-4 * eo), (e, eo)
