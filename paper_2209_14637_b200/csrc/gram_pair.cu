@@ -614,8 +614,9 @@ tsk_status gram_pair(Ctx* ctx, const GemmProblem& p) {
   // persistent clusters: no more than can be co-resident (the drift throttle assumes every unit of
   // a round is running)
   const int nsm = ctx->num_sms & ~1;
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
+  static int max_clusters_dev[64] = {};  // per device (0 = not queried yet)
+  int& max_clusters = max_clusters_dev[ctx->device & 63];
+  if (max_clusters <= 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nsm);
     cfg.blockDim = dim3(kThreads);
