@@ -14,8 +14,12 @@ for d0 in range(0, D, 250):
     tsk.sketch_gram(A, G64=G, accumulate=d0 > 0)
     del A
 torch.cuda.synchronize()
+ov = int(os.environ.get("OVERSAMPLE", "0"))
+opts = {"oversample": ov} if ov else None
+tsk.sketch_topk(G, c.k, opts=opts)
+torch.cuda.synchronize()
 t = time.time()
-S, lam, info, st = tsk.sketch_topk(G, c.k)
+S, lam, info, st = tsk.sketch_topk(G, c.k, opts=opts)
 torch.cuda.synchronize()
 el = time.time() - t
 w = torch.linalg.eigvalsh(G)
