@@ -42,3 +42,14 @@ def test_scw_worked_example(golden):
     assert scw.scw_error(A, S, g["r"]) == pytest.approx(g["error"], rel=1e-13)
     # Eckart-Young: the sketched error cannot beat the optimum
     assert scw.scw_error(A, S, g["r"]) >= scw.best_rank_r_error(A, g["r"])
+
+
+def test_projector_distance_spec_examples(golden):
+    """SPEC S:106-109 worked examples of the projector distance (reading c8):
+    U_k = e_1, S = e_2^T gives ||U_k U_k^T - S^T S||_F^2 = 2 (so the returned norm is sqrt 2);
+    identical 2-dim subspaces of R^3 give 0.  The transposed form S S^T - U_k^T U_k of P:150 is
+    1 x 1 (zero) on the first example and fails it."""
+    g = golden("projector_e1_e2.json")
+    Uk, S = np.array(g["U_k"]), np.array(g["S"])
+    assert tucker1.projector_distance(Uk.T, S) ** 2 == pytest.approx(g["distance_sq"], rel=1e-15)
+    assert tucker1.projector_distance(np.array(g["U_k_3"]).T, np.array(g["S_3"])) ** 2 == g["distance_sq_3"]

@@ -127,3 +127,25 @@ def test_k_out_of_range():
         tucker1.top_k_eigen(np.eye(3), 4)
     with pytest.raises(ValueError):
         tucker1.top_k_eigen(np.eye(3), 0)
+
+
+def test_projector_distance_principal_angles():
+    """Projector distance (reading c8) against closed forms that do not use the
+    projectors: for row-orthonormal k x m S1, S2, ||S1^T S1 - S2^T S2||_F^2 = 2k - 2||S1 S2^T||_F^2
+    = 2 sum_i sin^2(angle_i); in the plane, lines at angle t are sqrt(2)|sin t| apart.  A transposed
+    (k x k) or unsquared mutation fails every case."""
+    for t in (0.0, 0.3, np.pi / 4, 1.2, np.pi / 2):
+        S1 = np.array([[1.0, 0.0, 0.0]])
+        S2 = np.array([[np.cos(t), np.sin(t), 0.0]])
+        assert tucker1.projector_distance(S1, S2) == pytest.approx(np.sqrt(2) * abs(np.sin(t)), abs=1e-15)
+    rng = np.random.default_rng(11)
+    for k, m in ((1, 5), (3, 7), (4, 4), (6, 20)):
+        S1, S2 = _rand_rows(rng, k, m), _rand_rows(rng, k, m)
+        cos = np.linalg.svd(S1 @ S2.T, compute_uv=False)
+        want = 2.0 * np.sum(1.0 - np.clip(cos, 0, 1) ** 2)
+        assert tucker1.projector_distance(S1, S2) ** 2 == pytest.approx(want, rel=1e-10, abs=1e-12)
+        # the same subspace in another basis (SPEC S:110): 0
+        Q = np.linalg.qr(rng.standard_normal((k, k)))[0]
+        assert tucker1.projector_distance(S1, Q @ S1) < 1e-13
+    # nonzero value on a case the k x k form makes vanish
+    assert tucker1.projector_distance(_rand_rows(rng, 2, 6), _rand_rows(rng, 2, 6)) > 0.1
