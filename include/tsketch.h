@@ -52,7 +52,9 @@ typedef enum {
   TSK_ENCCL = -5,             /* NCCL library not loadable, or an NCCL call failed */
   TSK_EDEVICE = -6,           /* device is not compute capability 10.0 (sm_100a) */
   TSK_ENONFINITE = -7,        /* NaN/Inf in the training input, only with opts->check_finite */
-  TSK_ENULL = -8              /* a required pointer is NULL */
+  TSK_ENULL = -8,             /* a required pointer is NULL */
+  TSK_ENUMERIC = -9           /* numerical breakdown the fallbacks could not repair (e.g. the eigensolver's
+                                 Householder/Jacobi fallback failed repeatedly); not a CUDA fault */
 } tsk_status;
 
 /* Create a context on `device`, enqueueing on `cuda_stream` (a cudaStream_t; NULL = legacy
@@ -253,6 +255,14 @@ tsk_status tsk_gram_probe(tsk_ctx ctx, const float* A, int64_t D, int m, int n, 
    H [batch][p][p] fp64 symmetric (row-major); W [batch][p][p] eigenvectors as columns; lam
    [batch][p] eigenvalues, decreasing; sweeps [batch] (may be NULL) Jacobi sweeps used.  p <= 256. */
 tsk_status tsk_eig_probe(tsk_ctx ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps);
+
+/* Diagnostic: the dense symmetric eigensolver of the Rayleigh-Ritz step (Householder tridiagonalisation,
+   multisection bisection, twisted-factorisation eigenvectors; device pointers).  H [p][p] fp64 symmetric
+   (row-major, read as (H + H^T)/2); W [p][nw] the top nw eigenvectors as columns; lam [nw] decreasing;
+   flag (device int, may be NULL; set to 1 -- never cleared -- when max |W^T W - I| > orth_tol, i.e. an
+   eigenvalue cluster the vectors could not resolve).  1 <= nw <= p <= 256. */
+tsk_status tsk_syev_probe(tsk_ctx ctx, const double* H, int p, int nw, double* W, double* lam, int* flag,
+                          double orth_tol);
 
 #ifdef __cplusplus
 }

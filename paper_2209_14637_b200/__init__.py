@@ -27,13 +27,14 @@ TSK_WARN_RANK_CLAMPED = 1
 TSK_WARN_NOT_CONVERGED = 2
 STATUS_NAMES = {0: "TSK_OK", 1: "TSK_WARN_RANK_CLAMPED", 2: "TSK_WARN_NOT_CONVERGED", -1: "TSK_EINVAL",
                 -2: "TSK_ESHAPE", -3: "TSK_ENOMEM", -4: "TSK_ECUDA", -5: "TSK_ENCCL", -6: "TSK_EDEVICE", -7: "TSK_ENONFINITE",
-                -8: "TSK_ENULL"}
+                -8: "TSK_ENULL", -9: "TSK_ENUMERIC"}
 
 # every symbol include/tsketch.h declares (checked by tests/test_abi.py on CPU)
 EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_status_string", "tsk_launch_count",
             "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2",
             "sketch_train_two_sided", "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe",
-            "tsk_eig_probe", "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"]
+            "tsk_eig_probe", "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init",
+            "tsk_syev_probe"]
 
 
 class TskError(RuntimeError):
@@ -115,12 +116,13 @@ def lib() -> ctypes.CDLL:
         L.two_sided_scw_error.argtypes = [vp, f32p, i64, i32, i32, f32p, i32, f32p, i32, i32, f64p]
         L.tsk_gram_probe.argtypes = [vp, f32p, i64, i32, i32, f64p, i32, i32, i32]
         L.tsk_eig_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp]
+        L.tsk_syev_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp, ctypes.c_double]
         L.sketch_train_matrix_free.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, vp, vp]
         L.tsk_get_unique_id.argtypes = [vp]
         L.tsk_comm_init.argtypes = [vp, i32, i32, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
                   "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2", "sketch_train_two_sided",
-                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe",
+                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe", "tsk_syev_probe",
                   "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"):
             getattr(L, f).restype = i32
         _lib = L
@@ -346,6 +348,23 @@ def tsk_eig_probe(H: torch.Tensor, ctx: Optional[Context] = None):
     sw = torch.empty((B,), dtype=torch.int32, device=H.device)
     _check(lib().tsk_eig_probe(ctx.handle, _ptr(H), p, B, _ptr(W), _ptr(lam), _ptr(sw)), "tsk_eig_probe")
     return W, lam, sw
+
+
+def tsk_syev_probe(H: torch.Tensor, nw: Optional[int] = None, orth_tol: float = 1e-9,
+                   ctx: Optional[Context] = None):
+    """Diagnostic: the Rayleigh-Ritz eigensolver (include/tsketch.h).  H [p, p] fp64 cuda.
+    Returns (W [p, nw] eigenvectors as columns, lam [nw] decreasing, flag (int32 tensor, 1 = unresolved
+    cluster))."""
+    _need(H, torch.float64, "H", 2)
+    p = H.shape[0]
+    nw = p if nw is None else nw
+    ctx = ctx or context(H.device)
+    W = torch.empty((p, nw), dtype=torch.float64, device=H.device)
+    lam = torch.empty((nw,), dtype=torch.float64, device=H.device)
+    flag = torch.zeros((1,), dtype=torch.int32, device=H.device)
+    _check(lib().tsk_syev_probe(ctx.handle, _ptr(H), p, nw, _ptr(W), _ptr(lam), _ptr(flag), orth_tol),
+           "tsk_syev_probe")
+    return W, lam, flag
 
 
 # ---------------------------------------------------------------------------- two-sided variant

@@ -191,6 +191,7 @@ const char* tsk_status_string(tsk_status s) {
     case TSK_ENONFINITE: return "non-finite (NaN/Inf) entry in the training input";
     case TSK_EDEVICE: return "device is not sm_100 (B200)";
     case TSK_ENULL: return "required pointer is NULL";
+    case TSK_ENUMERIC: return "numerical breakdown the fallbacks could not repair";
   }
   return "unknown status";
 }
@@ -656,6 +657,16 @@ tsk_status tsk_eig_probe(tsk_ctx ctx, const double* H, int p, int batch, double*
   if (!is_device_ptr(H) || !is_device_ptr(W) || !is_device_ptr(lam) || (sweeps && !is_device_ptr(sweeps)))
     return TSK_EINVAL;
   return tsk::jacobi_eig_batched(&ctx->c, H, p, batch, W, lam, sweeps, 1e-13);
+}
+
+tsk_status tsk_syev_probe(tsk_ctx ctx, const double* H, int p, int nw, double* W, double* lam, int* flag,
+                          double orth_tol) {
+  if (!ctx) return TSK_ENULL;
+  if (!H || !W || !lam) return TSK_ENULL;
+  if (p < 1 || p > 256 || nw < 1 || nw > p) return TSK_EINVAL;
+  if (!is_device_ptr(H) || !is_device_ptr(W) || !is_device_ptr(lam) || (flag && !is_device_ptr(flag)))
+    return TSK_EINVAL;
+  return tsk::syev_top(&ctx->c, H, p, nw, W, nw, lam, flag, orth_tol);
 }
 
 }  // extern "C"

@@ -3,18 +3,25 @@
 // S* = (U^(1))_k^T: the first k left singular vectors of A_(1), i.e. the top-k eigenvectors
 // of G = A_(1) A_(1)^T (symmetric PSD, m x m).  The paper gives no algorithm for this step
 // (reading c4); we use:
-//   * m <= dense_max_m : one dense one-sided Jacobi eigensolve of G (fp64),
-//   * otherwise block subspace iteration with Rayleigh-Ritz (reading c15):
-//       Z = G Q            3xTF32 tensor-core product (gemm_tc.cu), fp64 result
-//       H = Q^T Z          fp64, symmetrised
-//       H = W diag(theta) W^T   one-sided Jacobi (jacobi.cu)
-//       X = Q W            Ritz vectors;  Y = Z W diag(1/theta)  (= G X / theta)
-//       residual_c = theta_c ||Y_c - X_c|| = ||G x_c - theta_c x_c||
-//       Q <- CholQR2(Y)    fp64 Cholesky QR, twice (Y is column-scaled: well conditioned)
-//     with block size p = k + oversample, stopped when every top-k Ritz pair has backward
-//     error ||G x_c - theta_c x_c|| <= tol * theta_1 (tol * ||G||_2), default 5e-7: about the
-//     3xTF32 G Q floor (~2-4e-7), and tight enough that the Ky Fan deficit of S stays ~1e-7 on
-//     the flat C3/C4 spectra (at 1e-6 it measured 1.5e-6).
+//   * m <= dense_max_m (default 256) or p = m: one dense eigensolve of G (syev.cu: Householder
+//     tridiagonalisation + bisection + twisted-factorisation eigenvectors; Jacobi fallback),
+//   * otherwise Chebyshev-filtered block subspace iteration (CheFSI) with Rayleigh-Ritz:
+//       0. dominant pre-pass: a few power steps on one vector; a pair that converges at a ratio
+//          <= 0.05 per step (a frame mean, C3/C4: lambda_1 / lambda_2 ~ 800) is locked and
+//          deflated from G before the block iteration (reading c15)
+//       1. Z = G'Y (G' = G minus the locked pairs), M = Y^T Y, CholQR: Q = Y diag(s) L^{-T},
+//          H = Q^T G' Q, (theta, W) = eig(H), X = Q W, G'X (all fp64)
+//       2. convergence: every wanted Ritz pair has ||G'x - theta x|| <= tol * theta_k, or -- where
+//          the k-th eigengap is below 1.05 -- the Kato-Temple estimate of the remaining Ky Fan
+//          deficit sum_i res_i^2 / (theta_i - theta_p) is <= tol/5 of the wanted energy still active
+//       3. lock the leading pairs with residual <= 1e-8 theta_i that sit >= 2x above theta_k,
+//          deflate them from G'
+//       4. Chebyshev filter of degree d on [a, b]: b = theta_p (the block's smallest Ritz value),
+//          a = max(0, mu - 2 sigma) from the mean / spread of the eigenvalues outside the block
+//          (trace and Frobenius norm of G minus the Ritz values); d is the largest degree keeping
+//          the filter's dynamic range T_d(x_top) <= 1e7 (the CholQR of step 1 then stays accurate)
+//     The products G'Y run in fp64 (a fused split-K SIMT kernel with the Chebyshev three-term
+//     combination in its epilogue) for m <= 2048 and on the 3xTF32 tensor cores above.
 // Output rows of S are the top-k Ritz vectors in decreasing theta order, each normalised
 // and sign-fixed so its largest-|entry| is positive (reading c5).
 #include <algorithm>
@@ -27,6 +34,9 @@
 #include "eig_kernels.cuh"
 #include "ptx.cuh"
 #include "tsk_internal.h"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace tsk {
 
@@ -68,33 +78,6 @@ __global__ void q_to_f32t_kernel(double* __restrict__ Q, int m, int p, int ms, f
   }
 }
 
-__global__ void inv_theta_kernel(const double* __restrict__ theta, int p, double* __restrict__ inv) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= p) return;
-  const double t = theta[c];
-  const double t0 = theta[0];
-  inv[c] = (fabs(t) > 1e-300 && fabs(t) > 1e-14 * fabs(t0)) ? 1.0 / t : (t0 != 0.0 ? 1.0 / t0 : 1.0);
-}
-
-// res[c] = theta_c * ||Y_c - X_c||  for c < k   (one block per column)
-__global__ void ritz_residual_kernel(const double* __restrict__ Y, const double* __restrict__ X, const double* theta,
-                                     int m, int p, double* __restrict__ res) {
-  const int c = blockIdx.x;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const double d = Y[(size_t)i * p + c] - X[(size_t)i * p + c];
-    s += d * d;
-  }
-  __shared__ double red[256];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) res[c] = fabs(theta[c]) * sqrt(red[0]);
-}
-
 // S[c][i] = sgn_c * V[i][c] / ||V_c||  for c < k  (V: [m][ldv]); sign makes the largest-|entry| positive
 __global__ void write_sketch_kernel(const double* __restrict__ V, int m, int ldv, float* __restrict__ S) {
   const int c = blockIdx.x;
@@ -132,34 +115,53 @@ __global__ void write_sketch_kernel(const double* __restrict__ V, int m, int ldv
 
 static inline unsigned nblk(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
-// ||G||_F^2 in a fixed order: gridDim.x CTAs sum contiguous slices (thread-strided partial sums,
-// tree reduction) into part[], then one CTA reduces part[] the same way (sum_kernel).  The
-// one-CTA version took 170 us at m = 1080.
-__global__ void fro2_part_kernel(const double* __restrict__ G, long long n, double* __restrict__ part) {
-  __shared__ double red[256];
+// fixed-order block reduction helpers --------------------------------------------------------
+__device__ __forceinline__ double warp_sum64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ||G||_F^2 and tr(G) in a fixed order: gridDim.x CTAs sum contiguous row ranges into part[2 * b],
+// then sum2_kernel reduces them.
+__global__ void fro_trace_part_kernel(const double* __restrict__ G, int m, double* __restrict__ part) {
+  __shared__ double red[2][32];
+  const long long n = (long long)m * m;
   const long long per = (n + gridDim.x - 1) / gridDim.x;
   const long long e0 = (long long)blockIdx.x * per, e1 = min(n, e0 + per);
-  double sacc = 0.0;
-  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) sacc += G[e] * G[e];
-  red[threadIdx.x] = sacc;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
+  double s2 = 0.0, tr = 0.0;
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const double g = G[e];
+    s2 = fma(g, g, s2);
+    if (e / m == e % m) tr += g;
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+  s2 = warp_sum64(s2);
+  tr = warp_sum64(tr);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s2;
+    red[1][threadIdx.x >> 5] = tr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
 }
-__global__ void sum_kernel(const double* __restrict__ x, long long n, double* __restrict__ out) {
-  __shared__ double red[1024];
-  double sacc = 0.0;
-  for (long long e = threadIdx.x; e < n; e += blockDim.x) sacc += x[e];
-  red[threadIdx.x] = sacc;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
+__global__ void sum2_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < nparts; ++i) {
+      a += part[2 * i];
+      b += part[2 * i + 1];
+    }
+    out[0] = a;
+    out[1] = b;
   }
-  if (threadIdx.x == 0) *out = red[0];
 }
 
 // Y[i][c] = S0[c][i] for c < k (Y: [m][p] fp64, S0: [k][m] fp32)
@@ -169,20 +171,6 @@ __global__ void init_cols_kernel(double* __restrict__ Y, int m, int p, const flo
   const int c = (int)(e / m), i = (int)(e % m);
   Y[(size_t)i * p + c] = (double)S0[(size_t)c * m + i];
 }
-
-// Y = Z diag(scale)   (m x p, row-major)
-__global__ void colscale_kernel(const double* __restrict__ Z, const double* __restrict__ scale, int m, int p,
-                                double* __restrict__ Y) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)m * p) return;
-  Y[idx] = Z[idx] * scale[idx % p];
-}
-
-// Q <- orthonormal basis of range(Y) by CholQR2 (fp64): C = Y^T Y = L L^T, Q1 = Y L^-T, twice.
-// Y arrives column-scaled (each column ~ G x_c / theta_c), so C is well conditioned and one
-// pass is already orthonormal to ~cond(Y)^2 eps; the second pass removes that residue.
-// flags[0..1] (device) receive the first failed pivot + 1 of each pass (0 = success): a failure
-// means rank(Y) < p, repaired by the caller.
 
 // G64[i][j] -= sum_t theta_t x_t[i] x_t[j]  (deflation of locked Ritz pairs; X: [m][ldx] columns t0..t1)
 __global__ void deflate_kernel(double* __restrict__ G, int m, const double* __restrict__ X, int ldx, int t0, int t1,
@@ -203,24 +191,6 @@ __global__ void cheb_step_kernel(const double* __restrict__ Z, const double* __r
   if (idx >= n) return;
   const double v = alpha * (Z[idx] - c * Yc[idx]);
   Yn[idx] = beta != 0.0 ? v - beta * Yp[idx] : v;
-}
-
-// column norms of Y (m x p) -> inverse norms (0 for a zero column); one block per column
-__global__ void inv_colnorm_kernel(const double* __restrict__ Y, int m, int p, double* __restrict__ inv) {
-  const int c = blockIdx.x;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const double v = Y[(size_t)i * p + c];
-    s += v * v;
-  }
-  __shared__ double red[256];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) inv[c] = red[0] > 0.0 ? 1.0 / sqrt(red[0]) : 0.0;
 }
 
 // copy columns [c0, c0+nc) of src [m][lds] to columns [d0, d0+nc) of dst [m][ldd]
@@ -245,15 +215,456 @@ static tsk_status cholqr_pass(Ctx* ctx, const double* Y, double* Q, int m, int p
   return trsm_rlt(ctx, Y, R, m, p, Q);
 }
 
-static tsk_status cholqr1(Ctx* ctx, const double* Y, double* Q, int m, int p, double* C, double* R, int* flags) {
-  return cholqr_pass(ctx, Y, Q, m, p, C, R, flags);
-}
-
 tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int m, int p, double* C, double* R,
-                          int* flags) {
+                   int* flags) {
   tsk_status st;
   if ((st = cholqr_pass(ctx, Y, Q1, m, p, C, R, flags)) != TSK_OK) return st;
   return cholqr_pass(ctx, Q1, Q, m, p, C, R, flags + 1);
+}
+
+// ---------------------------------------------------------------- fused fp64 product G'Y
+// Out[i][c] = alpha * sum_l G[i][l] Y[l][c] + beta * Y[i][c] + gamma * Yp[i][c]   (i < m, c < q)
+// (Y, Yp, Out: [m][ldy]; Yp may be null when gamma == 0).  CTA tile 64 rows x 16 JN columns,
+// 256 threads (16 x 16; thread (ty, tx) owns rows ty + 16 a, a < 4, and columns tx + 16 j, j < JN),
+// K in chunks of 16 through shared memory with the next chunk prefetched into registers.
+// Split-K over blockIdx.y: the S CTAs of a row tile form one thread-block cluster; each leaves its
+// partial tile in shared memory and, after a cluster barrier, CTA r sums rows r, r + S, ... of all
+// S partials over DSMEM in split order and applies the epilogue -- deterministic, no global
+// round trip.  This is the Chebyshev filter step (the three-term axpy fused into the
+// product epilogue) and the Rayleigh-Ritz product Z = G'Y.
+constexpr int kGqBM = 64, kGqKC = 16, kGqThreads = 256;
+template <int JN>
+__global__ void __launch_bounds__(kGqThreads) gq_f64_kernel(const double* __restrict__ G, int m, int ldg,
+                                                            const double* __restrict__ Y,
+                                                            const double* __restrict__ Yp, int q, int ldy,
+                                                            double alpha, double beta, double gamma,
+                                                            double* __restrict__ Out, int splits) {
+  constexpr int BN = 16 * JN;
+  constexpr int NA = kGqBM * kGqKC / kGqThreads;  // G elements per thread per chunk (4)
+  constexpr int NB = kGqKC * BN / kGqThreads;     // Y elements per thread per chunk (2 JN)
+  extern __shared__ double gq_sm[];
+  double* As = gq_sm;                            // [KC][BM + 1]
+  double* Bs = As + kGqKC * (kGqBM + 1);         // [KC][BN]
+  double* Ps = Bs + kGqKC * BN;                  // [BM][BN] this CTA's partial tile
+  cg::cluster_group cluster = cg::this_cluster();
+  const int tile = blockIdx.x, sp = blockIdx.y;
+  const int i0 = tile * kGqBM;
+  const int k0 = (int)((long long)sp * m / splits), k1 = (int)((long long)(sp + 1) * m / splits);
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;  // 16 x 16
+  double ra[NA], rb[NB];
+  auto fetch = [&](int kk) {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int e = tid + u * kGqThreads;
+      const int r = e / kGqKC, kc = e % kGqKC;
+      const int row = i0 + r, col = kk + kc;
+      ra[u] = (row < m && col < k1) ? __ldg(G + (size_t)row * ldg + col) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int e = tid + u * kGqThreads;
+      const int kc = e / BN, c = e % BN;
+      rb[u] = (kk + kc < k1 && c < q) ? __ldg(Y + (size_t)(kk + kc) * ldy + c) : 0.0;
+    }
+  };
+  auto stage = [&]() {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int e = tid + u * kGqThreads;
+      As[(e % kGqKC) * (kGqBM + 1) + e / kGqKC] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int e = tid + u * kGqThreads;
+      Bs[(e / BN) * BN + e % BN] = rb[u];
+    }
+  };
+  double acc[4][JN];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int j = 0; j < JN; ++j) acc[a][j] = 0.0;
+  if (k0 < k1) {
+    fetch(k0);
+    stage();
+  }
+  __syncthreads();
+  for (int kk = k0; kk < k1; kk += kGqKC) {
+    const bool more = kk + kGqKC < k1;
+    if (more) fetch(kk + kGqKC);  // in flight during the products below
+#pragma unroll
+    for (int kc = 0; kc < kGqKC; ++kc) {
+      double av[4], bv[JN];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kc * (kGqBM + 1) + ty + 16 * a];
+#pragma unroll
+      for (int j = 0; j < JN; ++j) bv[j] = Bs[kc * BN + tx + 16 * j];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int j = 0; j < JN; ++j) acc[a][j] = fma(av[a], bv[j], acc[a][j]);
+    }
+    __syncthreads();
+    if (more) {
+      stage();
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int j = 0; j < JN; ++j) Ps[(ty + 16 * a) * BN + tx + 16 * j] = acc[a][j];
+  cluster.sync();
+  // CTA sp of the cluster reduces rows sp, sp + S, ... of the tile over the S partials (fixed order)
+  for (int e = tid; e < kGqBM * BN; e += kGqThreads) {
+    const int r = e / BN, c = e % BN;
+    if (r % splits != sp) continue;
+    const int row = i0 + r;
+    if (row >= m || c >= q) continue;
+    double sacc = 0.0;
+    for (int t = 0; t < splits; ++t) sacc += cluster.map_shared_rank(Ps, t)[e];
+    double v = alpha * sacc;
+    if (beta != 0.0) v = fma(beta, Y[(size_t)row * ldy + c], v);
+    if (gamma != 0.0) v = fma(gamma, Yp[(size_t)row * ldy + c], v);
+    Out[(size_t)row * ldy + c] = v;
+  }
+  cluster.sync();  // no CTA leaves while its partial tile may still be read
+}
+
+template <int JN>
+static cudaError_t launch_gq(int mt, int splits, cudaStream_t s, const double* G, int m, const double* Y,
+                             const double* Yp, int q, int ldy, double alpha, double beta, double gamma, double* Out) {
+  const size_t smem = (size_t)(kGqKC * (kGqBM + 1) + kGqKC * 16 * JN + kGqBM * 16 * JN) * sizeof(double);
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
+    cudaFuncSetAttribute(gq_f64_kernel<JN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gq_f64_kernel<JN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr |= device_bit();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(mt, splits, 1);
+  cfg.blockDim = dim3(kGqThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = splits;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gq_f64_kernel<JN>, G, m, m, Y, Yp, q, ldy, alpha, beta, gamma, Out, splits);
+}
+
+// Out = alpha G Y + beta Y + gamma Yp for Y [m][ldy] with q <= 128 columns (fp64)
+static tsk_status gq_f64(Ctx* ctx, const double* G, int m, const double* Y, const double* Yp, int q, int ldy,
+                         double alpha, double beta, double gamma, double* Out) {
+  if (q < 1 || q > 128) return TSK_EINVAL;
+  const int JN = (q + 15) / 16;
+  const int mt = (m + kGqBM - 1) / kGqBM;
+  // split K so that ~one wave of CTAs covers the SMs (cluster of <= 8), >= 64 of K per split
+  const int splits = std::max(1, std::min(std::min((ctx->num_sms + mt - 1) / mt, std::max(1, m / 64)), 8));
+  cudaStream_t s = ctx->stream;
+  cudaError_t e;
+  switch (JN) {
+    case 1: e = launch_gq<1>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 2: e = launch_gq<2>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 3: e = launch_gq<3>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 4: e = launch_gq<4>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 5: e = launch_gq<5>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 6: e = launch_gq<6>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 7: e = launch_gq<7>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    default: e = launch_gq<8>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+  }
+  ctx->count_launch();
+  if (e != cudaSuccess) {
+    if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gq_f64: %s\n", cudaGetErrorString(e));
+    cudaGetLastError();
+    return TSK_ECUDA;
+  }
+  return launch_status("gq_f64");
+}
+
+// Out = alpha Z + beta Y + gamma Yp  (elementwise over n; Yp may be null when gamma == 0)
+__global__ void axpby3_kernel(const double* __restrict__ Z, const double* __restrict__ Y,
+                              const double* __restrict__ Yp, long long n, double alpha, double beta, double gamma,
+                              double* __restrict__ Out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  double v = alpha * Z[idx];
+  if (beta != 0.0) v = fma(beta, Y[idx], v);
+  if (gamma != 0.0) v = fma(gamma, Yp[idx], v);
+  Out[idx] = v;
+}
+
+// ---------------------------------------------------------------- dominant pre-pass (power steps)
+// w = G v, one warp per row (coalesced row reads), plus the per-row terms of v.w and ||w||^2
+__global__ void matvec_rows_kernel(const double* __restrict__ G, int m, const double* __restrict__ v,
+                                   double* __restrict__ w) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  const double* row = G + (size_t)warp * m;
+  double s = 0.0;
+  for (int j = lane; j < m; j += 32) s = fma(row[j], v[j], s);
+  s = warp_sum64(s);
+  if (lane == 0) w[warp] = s;
+}
+// one CTA: theta = v.w, res = ||w - theta v||, v <- w / ||w||; out[0..1] = theta, res (history in out[2*step..])
+__global__ void power_update_kernel(double* __restrict__ v, const double* __restrict__ w, int m, double* __restrict__ out,
+                                    int step) {
+  __shared__ double red[3][32];
+  __shared__ double th_s, nw_s;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double a = 0.0, b = 0.0;
+  for (int i = tid; i < m; i += nt) {
+    a = fma(v[i], w[i], a);
+    b = fma(w[i], w[i], b);
+  }
+  a = warp_sum64(a);
+  b = warp_sum64(b);
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = a;
+    red[1][tid >> 5] = b;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int k = 0; k < nt / 32; ++k) {
+      sa += red[0][k];
+      sb += red[1][k];
+    }
+    th_s = sa;
+    nw_s = sqrt(sb);
+  }
+  __syncthreads();
+  const double th = th_s;
+  double c = 0.0;
+  for (int i = tid; i < m; i += nt) {
+    const double r = w[i] - th * v[i];
+    c = fma(r, r, c);
+  }
+  c = warp_sum64(c);
+  if ((tid & 31) == 0) red[2][tid >> 5] = c;
+  __syncthreads();
+  if (tid == 0) {
+    double sc = 0.0;
+    for (int k = 0; k < nt / 32; ++k) sc += red[2][k];
+    out[2 * step] = th;
+    out[2 * step + 1] = sqrt(sc);
+  }
+  const double inv = nw_s > 0.0 ? 1.0 / nw_s : 0.0;
+  __syncthreads();  // all reads of v above precede the overwrite
+  for (int i = tid; i < m; i += nt) v[i] = w[i] * inv;
+}
+
+// global -> shared copy of n doubles, 8 loads in flight per thread
+__device__ __forceinline__ void copy_to_shared_f64(double* dst, const double* __restrict__ src, int n, int tid,
+                                                   int nthreads) {
+  int e = tid;
+  for (; e + 7 * nthreads < n; e += 8 * nthreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + e + u * nthreads);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dst[e + u * nthreads] = v[u];
+  }
+  for (; e < n; e += nthreads) dst[e] = __ldg(src + e);
+}
+
+// ---------------------------------------------------------------- Cholesky for the RR (CholQR)
+// M [p][p] (Gram of the block Y) -> column scaling s_i = 1/sqrt(M_ii), Cholesky of S M S = L L^T
+// (right-looking, deferred column scaling: one barrier per step); outputs L [p][p] (lower, row-
+// major, upper part untouched), rinv [p] = 1 / L_ii and s [p].  A pivot <= rel_tol (of the unit
+// scaled diagonal) sets flag[0] = step + 1: the block is numerically rank deficient and the caller
+// falls back (shifted CholQR, then Householder QR).  shift (>= 0) is added to the scaled diagonal:
+// the shifted CholQR of Fukaya et al., which cannot break down for cond(Y) up to ~1/sqrt(eps).
+// One CTA, 512 threads (32 x 16), the factor in shared memory.
+constexpr int kCiThreads = 512;
+__global__ void __launch_bounds__(kCiThreads) chol_scale_kernel(const double* __restrict__ M, int p,
+                                                                double rel_tol, double shift, double* __restrict__ L,
+                                                                double* __restrict__ rinv_out,
+                                                                double* __restrict__ s_out,
+                                                                int* __restrict__ flag) {
+  extern __shared__ double ci_sm[];
+  const int ld = p | 1;
+  double* A = ci_sm;  // [p][ld]
+  __shared__ double s[256];
+  __shared__ int fail;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < p; i += nt) {
+    const double d = M[(size_t)i * p + i];
+    const double si = d > 0.0 ? 1.0 / sqrt(d) : 0.0;
+    s[i] = si;
+    s_out[i] = si;
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (int e = tid; e < p * p; e += nt) {
+    const int i = e / p, j = e - (e / p) * p;
+    if (j <= i) A[i * ld + j] = M[e] * s[i] * s[j] + (i == j ? shift : 0.0);
+  }
+  __syncthreads();
+  const int ty = tid >> 4, tx = tid & 15;  // 32 x 16
+  for (int j = 0; j < p; ++j) {
+    double d = A[j * ld + j];
+    if (!(d > rel_tol)) {  // uniform (every thread reads the same pivot); the caller falls back
+      if (tid == 0 && fail == 0) fail = j + 1;
+      d = 1.0;
+    }
+    const double inv_d = __drcp_rn(d);
+    for (int i = j + 1 + ty; i < p; i += 32) {
+      const double f = A[i * ld + j] * inv_d;
+      double* row = A + i * ld;
+      for (int l = j + 1 + tx; l <= i; l += 16) row[l] = fma(-f, A[l * ld + j], row[l]);
+    }
+    __syncthreads();
+  }
+  // L_jj = sqrt(d_j), L_ij = A_ij / sqrt(d_j)
+  for (int j = tid; j < p; j += nt) {
+    const double dj = A[j * ld + j];
+    const double r = dj > 0.0 ? sqrt(dj) : 1.0;
+    rinv_out[j] = 1.0 / r;
+    s[j] = r;  // reuse: sqrt(d_j)
+  }
+  __syncthreads();
+  for (int e = tid; e < p * p; e += nt) {
+    const int i = e / p, j = e - (e / p) * p;
+    if (j < i) L[e] = A[i * ld + j] / s[j];
+    else if (j == i) L[e] = s[j];
+  }
+  if (tid == 0 && fail) flag[0] = fail;
+}
+
+// Q = (Y diag(s)) L^{-T} and GQ = (Z diag(s)) L^{-T}: row-parallel forward substitution
+// q L^T = y (q_c = (y_c s_c - sum_{a<c} q_a L_ca) / L_cc), one thread per row of Y or Z (rows
+// [0, m) of Y then [m, 2m) of Z), L and the thread's q row in shared memory.
+constexpr int kTrsmRows = 64;
+__global__ void __launch_bounds__(kTrsmRows) trsm2_kernel(const double* __restrict__ Y, const double* __restrict__ Z,
+                                                          const double* __restrict__ s, const double* __restrict__ L,
+                                                          const double* __restrict__ rinv, int m, int p,
+                                                          double* __restrict__ Q, double* __restrict__ GQ) {
+  extern __shared__ double tr_sm[];
+  const int ldq = p | 1;
+  double* Ls = tr_sm;                          // [p][p]
+  double* qs = tr_sm + (size_t)p * p;          // [kTrsmRows][ldq]
+  double* ss = qs + (size_t)kTrsmRows * ldq;   // [p] s
+  double* rs = ss + p;                         // [p] 1 / L_cc
+  copy_to_shared_f64(Ls, L, p * p, threadIdx.x, blockDim.x);
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    ss[c] = s[c];
+    rs[c] = rinv[c];
+  }
+  __syncthreads();
+  const int row = blockIdx.x * kTrsmRows + threadIdx.x;
+  if (row >= 2 * m) return;
+  const double* y = row < m ? Y + (size_t)row * p : Z + (size_t)(row - m) * p;
+  double* out = row < m ? Q + (size_t)row * p : GQ + (size_t)(row - m) * p;
+  double* q = qs + (size_t)threadIdx.x * ldq;
+#pragma unroll 8
+  for (int c = 0; c < p; ++c) q[c] = __ldg(y + c) * ss[c];  // independent loads, one latency
+  for (int c = 0; c < p; ++c) {
+    const double* Lc = Ls + (size_t)c * p;
+    double a0 = q[c], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int a = 0;
+    for (; a + 3 < c; a += 4) {
+      a0 = fma(-q[a], Lc[a], a0);
+      a1 = fma(-q[a + 1], Lc[a + 1], a1);
+      a2 = fma(-q[a + 2], Lc[a + 2], a2);
+      a3 = fma(-q[a + 3], Lc[a + 3], a3);
+    }
+    for (; a < c; ++a) a0 = fma(-q[a], Lc[a], a0);
+    q[c] = ((a0 + a1) + (a2 + a3)) * rs[c];
+  }
+  for (int c = 0; c < p; ++c) out[c] = q[c];
+}
+
+// ---------------------------------------------------------------- Householder QR (fallback)
+// Q = first p columns of the orthogonal factor of Y (m x p, row-major, in place), by Householder
+// reflections (LAPACK dgeqr2 + dorg2r order), one CTA.  Used when the Cholesky of the block Gram
+// breaks down (numerically rank-deficient block, e.g. rank(G) < p): Householder QR has no such
+// failure mode -- a zero column yields a trivial reflector and the factor still has orthonormal
+// columns (PAPER.md:191 licenses any QR for the orthogonalisation).  Scratch: tau [p], V [m][p].
+constexpr int kHqrThreads = 1024;
+__global__ void __launch_bounds__(kHqrThreads) hqr_kernel(double* __restrict__ Y, int m, int p,
+                                                          double* __restrict__ V, double* __restrict__ tau) {
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  auto block_sum = [&](double v) -> double {
+    v = warp_sum64(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    return t;
+  };
+  // factorisation: reflector j from column j, rows j..m-1; v stored in V[:, j] (v_j = 1)
+  for (int j = 0; j < p; ++j) {
+    double s2 = 0.0;
+    for (int i = j + 1 + tid; i < m; i += nt) {
+      const double x = Y[(size_t)i * p + j];
+      s2 = fma(x, x, s2);
+    }
+    s2 = block_sum(s2);
+    const double alpha = Y[(size_t)j * p + j];
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (s2 > 0.0) {
+      const double mu = sqrt(fma(alpha, alpha, s2));
+      beta = alpha <= 0.0 ? mu : -mu;
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = j + tid; i < m; i += nt) V[(size_t)i * p + j] = i == j ? 1.0 : Y[(size_t)i * p + j] * scal;
+    if (tid == 0) tau[j] = t;
+    __syncthreads();
+    // apply H_j to columns c > j: y_c -= t v (v^T y_c); one warp per column
+    if (t != 0.0)
+      for (int c = j + 1 + warp; c < p; c += nw) {
+        double d = 0.0;
+        for (int i = j + lane; i < m; i += 32) d = fma(V[(size_t)i * p + j], Y[(size_t)i * p + c], d);
+        d = warp_sum64(d) * t;
+        for (int i = j + lane; i < m; i += 32) Y[(size_t)i * p + c] = fma(-d, V[(size_t)i * p + j], Y[(size_t)i * p + c]);
+      }
+    __syncthreads();
+  }
+  // Q = H_0 ... H_{p-1} [I_p; 0], accumulated backwards in Y
+  for (long long e = tid; e < (long long)m * p; e += nt) {
+    const int i = (int)(e / p), c = (int)(e % p);
+    Y[e] = i == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = p - 1; j >= 0; --j) {
+    const double t = tau[j];
+    if (t != 0.0)
+      for (int c = j + warp; c < p; c += nw) {
+        double d = 0.0;
+        for (int i = j + lane; i < m; i += 32) d = fma(V[(size_t)i * p + j], Y[(size_t)i * p + c], d);
+        d = warp_sum64(d) * t;
+        for (int i = j + lane; i < m; i += 32) Y[(size_t)i * p + c] = fma(-d, V[(size_t)i * p + j], Y[(size_t)i * p + c]);
+      }
+    __syncthreads();
+  }
+}
+
+// res[c] = ||GX_c - theta_c X_c|| for c < gridDim.x (X, GX: [m][ld]); one CTA per column
+__global__ void ritz_res_kernel(const double* __restrict__ GX, const double* __restrict__ X, int ld,
+                                const double* __restrict__ theta, int m, double* __restrict__ res) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  const double th = theta[c];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double d = GX[(size_t)i * ld + c] - th * X[(size_t)i * ld + c];
+    s = fma(d, d, s);
+  }
+  s = warp_sum64(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    res[c] = sqrt(t);
+  }
 }
 
 tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
@@ -261,101 +672,106 @@ tsk_status topk_eigen(Ctx* ctx, const double* G64, int m, int k, float* S, doubl
   return topk_eigen_ex(ctx, G64, m, k, S, lambda, o, info, 0, nullptr);
 }
 
-// f64_products: G Q in fp64 (SIMT GEMM on the fp64 master copy) instead of 3xTF32 -- for small
-// dense matrices (the matrix-free sketch's Rayleigh-Ritz matrix, m <= 256) where fp64 is cheap and
-// the one-CTA Jacobi would have to leave shared memory (m > 116); tolerances scale accordingly.
-// X64 (optional, device [m][k] fp64): the output eigenvectors as columns, before the fp32 rounding
-// of S (same order; sign rule applied to S only).
+// dense path: all of G in one small eigensolve (m <= 256)
+static tsk_status topk_dense(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
+                             tsk_train_info* info, double* X64) {
+  cudaStream_t s = ctx->stream;
+  double* W = reinterpret_cast<double*>(ctx->workspace(WS_EIG_A, (size_t)m * m * 8));
+  double* lam = reinterpret_cast<double*>(ctx->workspace(WS_EIG_SMALL, (size_t)m * 8 + 64));
+  int* flag = reinterpret_cast<int*>(lam + m);
+  double* hostbuf = reinterpret_cast<double*>(ctx->pinned((size_t)(m + 16) * 8));
+  if (!W || !lam || !hostbuf) return TSK_ENOMEM;
+  tsk_status st;
+  // k + 1 pairs (the (k+1)-th for the eigengap estimate)
+  const int nw = std::min(m, k + 1);
+  cudaMemsetAsync(flag, 0, sizeof(int), s);
+  if ((st = syev_top(ctx, G64, m, nw, W, m, lam, flag, 1e-9)) != TSK_OK) return st;
+  int hf = 0;
+  if (cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return TSK_ECUDA;
+  if (hf && (st = jacobi_eig_batched(ctx, G64, m, 1, W, lam)) != TSK_OK) return st;  // clustered spectrum
+  write_sketch_kernel<<<k, 256, 0, s>>>(W, m, m, S);
+  ctx->count_launch();
+  if (X64) {
+    copy_cols_kernel<<<nblk((long long)m * k, 256), 256, 0, s>>>(W, m, 0, X64, k, 0, m, k);
+    ctx->count_launch();
+  }
+  if (lambda) cudaMemcpyAsync(lambda, lam, (size_t)k * 8, cudaMemcpyDeviceToDevice, s);
+  if (info) {
+    info->iters = 0;
+    cudaMemcpyAsync(hostbuf, lam, (size_t)nw * 8, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return TSK_ECUDA;
+    double kf = 0;
+    for (int c = 0; c < k; ++c) kf += hostbuf[c];
+    info->kyfan = kf;
+    info->max_resid = 0.0;
+    info->gap_est = (k < m && hostbuf[k] > 0.0) ? hostbuf[k - 1] / hostbuf[k] : INFINITY;
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
+}
+
+// f64_products: force fp64 G Q products for every m (the tensor-core path is otherwise used for
+// m > 2048).  X64 (optional, device [m][k] fp64): the output eigenvectors as columns, before the
+// fp32 rounding of S (same order; sign rule applied to S only).
 tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, double* lambda,
                          const tsk_train_opts* o, tsk_train_info* info, int f64_products, double* X64) {
   if (m < 1 || k < 1 || k > m) return TSK_EINVAL;
   tsk_train_opts opt{};
   if (o) opt = *o;
-  const bool f64 = f64_products != 0;
-  const int dense_max = opt.dense_max_m > 0 ? opt.dense_max_m : (f64 ? 116 : 256);
+  const int dense_max = opt.dense_max_m > 0 ? opt.dense_max_m : 256;
   const int max_iters = opt.max_iters > 0 ? opt.max_iters : 300;
-  const double tol = opt.tol > 0 ? opt.tol : (f64 ? 1e-11 : 5e-7);
-
-  // block size p = k + 16 by default: measured on C3/C4 spectra (flat near k), larger blocks cut
-  // iterations less than they raise the cost of each p x p Rayleigh-Ritz solve
+  const double tol = opt.tol > 0 ? opt.tol : 1e-6;
+  const double kf_tol = 0.2 * tol;
+  const bool trace = getenv("TSK_EIG_TRACE") != nullptr;
   int p = opt.oversample > 0 ? k + opt.oversample : k + 16;
   p = std::min(p, m);
+  if (m <= dense_max || p >= m) {
+    if (m > 256) return TSK_EINVAL;
+    return topk_dense(ctx, G64, m, k, S, lambda, info, X64);
+  }
+  if (p > 128) return TSK_EINVAL;
+  const bool tc = !f64_products && m > 2048 && !getenv("TSK_EIG_F64");
   cudaStream_t s = ctx->stream;
   tsk_status st;
 
-  if (m <= dense_max || p >= m || (!f64 && m <= 256)) {
-    if (m > 256) return TSK_EINVAL;
-    double* W = reinterpret_cast<double*>(ctx->workspace(WS_EIG_A, (size_t)m * m * 8));
-    double* lam = reinterpret_cast<double*>(ctx->workspace(WS_EIG_SMALL, (size_t)m * 8 + 64));
-    if (!W || !lam) return TSK_ENOMEM;
-    if ((st = jacobi_eig_batched(ctx, G64, m, 1, W, lam)) != TSK_OK) return st;
-    write_sketch_kernel<<<k, 256, 0, s>>>(W, m, m, S);
-    ctx->count_launch();
-    if (X64) {
-      copy_cols_kernel<<<nblk((long long)m * k, 256), 256, 0, s>>>(W, m, 0, X64, k, 0, m, k);
-      ctx->count_launch();
-    }
-    if (lambda) cudaMemcpyAsync(lambda, lam, (size_t)k * 8, cudaMemcpyDeviceToDevice, s);
-    if (info) {
-      info->iters = 0;
-      std::vector<double> h(k);
-      cudaMemcpyAsync(h.data(), lam, (size_t)k * 8, cudaMemcpyDeviceToHost, s);
-      cudaStreamSynchronize(s);
-      double kf = 0;
-      for (double v : h) kf += v;
-      info->kyfan = kf;
-      info->max_resid = 0.0;
-      double lk1 = 0.0;
-      if (k < m) cudaMemcpy(&lk1, lam + k, 8, cudaMemcpyDeviceToHost);
-      info->gap_est = lk1 > 0.0 ? h[k - 1] / lk1 : INFINITY;
-    }
-    return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
-  }
-
   const int ms = (m + 3) & ~3;
   const size_t mp = (size_t)m * p;
-  // workspace carve-up
+  const size_t pq = (size_t)p * (p + 1) + 8;  // one small p x p matrix (room for an odd pitch)
+  // workspace: 8 blocks [m][p] fp64 (rotated by pointer), Gd [m][m], small matrices
   double* big = reinterpret_cast<double*>(ctx->workspace(WS_EIG_A, mp * 8 * 8));
-  double* small = reinterpret_cast<double*>(ctx->workspace(WS_EIG_B, ((size_t)p * p * 4 + p * 12) * 8 + 256));
-  float* G32 = reinterpret_cast<float*>(ctx->workspace(WS_EIG_G32, (size_t)m * ms * 4));
-  float* Qt = reinterpret_cast<float*>(ctx->workspace(WS_EIG_Q32, (size_t)p * ms * 4));
+  double* small = reinterpret_cast<double*>(ctx->workspace(WS_EIG_B, (pq * 6 + (size_t)p * 16 + 512) * 8));
   double* Gd = reinterpret_cast<double*>(ctx->workspace(WS_EIG_C, (size_t)m * m * 8));
-  double* hostbuf = reinterpret_cast<double*>(ctx->pinned((size_t)(4 * p + 16) * 8));
-  if (!big || !small || !G32 || !Qt || !Gd || !hostbuf) return TSK_ENOMEM;
-  double *Q = big, *Z = big + mp, *X = big + 2 * mp, *Y = big + 3 * mp, *Q1 = big + 4 * mp;
-  double *Y0 = big + 5 * mp, *Y1 = big + 6 * mp, *Xl = big + 7 * mp;  // Xl: locked Ritz vectors [m][p]
-  double *H = small, *W = small + (size_t)p * p, *C = small + 2 * (size_t)p * p, *Rinv = small + 3 * (size_t)p * p;
-  double *theta = small + 4 * (size_t)p * p, *invt = theta + p, *res = theta + 2 * p, *thl = theta + 3 * p;
-  double* ncol = theta + 4 * p;
-  int* flags = reinterpret_cast<int*>(theta + 6 * p);
+  float* G32 = tc ? reinterpret_cast<float*>(ctx->workspace(WS_EIG_G32, (size_t)m * ms * 4)) : nullptr;
+  float* Qt = tc ? reinterpret_cast<float*>(ctx->workspace(WS_EIG_Q32, (size_t)p * ms * 4)) : nullptr;
+  double* hostbuf = reinterpret_cast<double*>(ctx->pinned((size_t)(4 * p + 64) * 8));
+  if (!big || !small || !Gd || (tc && (!G32 || !Qt)) || !hostbuf) return TSK_ENOMEM;
+  // block buffers: Y (the block entering a Rayleigh-Ritz step), Z = G'Y, X / GX (Ritz vectors and
+  // G' times them), Xl (locked vectors, ld p), T (product / projection scratch), F0, F1 (free)
+  double* Y = big;
+  double* Z = big + mp;
+  double* X = big + 2 * mp;
+  double* GX = big + 3 * mp;
+  double* F0 = big + 4 * mp;
+  double* F1 = big + 5 * mp;
+  double* Xl = big + 6 * mp;
+  double* T = big + 7 * mp;
+  double *M = small, *Rs = small + pq, *H = small + 2 * pq, *W = small + 3 * pq, *Cn = small + 4 * pq;
+  double* Cl = small + 5 * pq;
+  double *theta = small + 6 * pq, *res = theta + p, *thl = theta + 2 * p, *pw = theta + 3 * p;
+  double* scal = theta + 16 * p;  // [0] ||G||_F^2, [1] tr G
+  int* flags = reinterpret_cast<int*>(scal + 64);  // [0] Cholesky breakdown, [1] syev non-orthogonal
+  double* hqr_tau = scal + 96;
+  int products = 0;
 
-  // The iteration works on the deflated Gram G' = G - sum_locked theta_t x_t x_t^T (fp64 master
-  // copy Gd, fp32 copy G32 for the tensor-core products).
+  // G' = G (fp64 copy, deflated as pairs lock); fp32 copy for the tensor-core products
   cudaMemcpyAsync(Gd, G64, (size_t)m * m * 8, cudaMemcpyDeviceToDevice, s);
-  g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(Gd, m, ms, G32);
-  hash_fill_kernel<<<nblk((long long)mp, 256), 256, 0, s>>>(Y, m, p, 0x5EEDull, 1.0, 0);
-  ctx->count_launch(2);
-  if (opt.init_S) {  // warm start: the first k columns of the starting block are the given rows
-    init_cols_kernel<<<nblk((long long)m * k, 256), 256, 0, s>>>(Y, m, p, opt.init_S, k);
+  auto refresh_g32 = [&]() {
+    if (!tc) return;
+    g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(Gd, m, ms, G32);
     ctx->count_launch();
-  }
-  cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
-  if ((st = cholqr2(ctx, Y, Q1, Q, m, p, C, Rinv, flags)) != TSK_OK) return st;
-  // Working-precision floor of the Ritz residual: the 3xTF32 G Q products carry an error of
-  // ~1e-8 ||G||_F (measured at C5, where ||G||_F / theta_1 = 61 and the residual stalls at 6e-7);
-  // the requested tol is raised to 4x that floor, and a Ky Fan energy that no longer changes
-  // (< 1e-12 relative over two outer iterations) also ends the iteration.
-  fro2_part_kernel<<<128, 256, 0, s>>>(G64, (long long)m * m, X);  // X: scratch until the loop
-  sum_kernel<<<1, 128, 0, s>>>(X, 128, ncol);
-  ctx->count_launch(2);
-  double gfro2 = 0.0;
-  cudaMemcpyAsync(&gfro2, ncol, 8, cudaMemcpyDeviceToHost, s);
-  if (cudaStreamSynchronize(s) != cudaSuccess) return TSK_ECUDA;
-  const double gfro = std::sqrt(std::max(gfro2, 0.0));
-  double kyfan_prev = -1.0, kf_change_prev = -1.0;
-  int kyfan_still = 0;
-  constexpr double kKyFanTol = 5e-7;  // estimated remaining Ky Fan deficit at the stop (half the 1e-6 check)
-
+  };
+  refresh_g32();
   GemmProblem gp;
   gp.X = G32;
   gp.Y = Qt;
@@ -366,217 +782,298 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
   gp.x_slice_stride = (long long)m * ms;
   gp.y_row_stride = ms;
   gp.min_chunks_per_unit = 2;
-  gp.chain = 1;  // short TMEM chains: the eigensolver needs G Q to ~3e-7, not ~1e-6
-
-  // Z = G' B for an m x pa fp64 block B (fp32 copy for the tensor cores; B <- fp64(fp32(B)))
-  auto gq = [&](double* B, int pa) -> tsk_status {
-    if (f64) return gemm_nn_f64(ctx, Gd, m, 0, B, pa, 0, m, m, pa, 1, nullptr, Z, pa, 0);
-    q_to_f32t_kernel<<<nblk((long long)pa * ms, 256), 256, 0, s>>>(B, m, pa, ms, Qt);
+  gp.chain = 1;
+  // Out = alpha G' B + beta B + gamma Bp  for B [m][q] (Out distinct from B, Bp; T is scratch)
+  auto product = [&](double* B, double* Bp, int q, double alpha, double beta, double gamma,
+                     double* Out) -> tsk_status {
+    ++products;
+    if (!tc) return gq_f64(ctx, Gd, m, B, Bp, q, q, alpha, beta, gamma, Out);
+    q_to_f32t_kernel<<<nblk((long long)q * ms, 256), 256, 0, s>>>(B, m, q, ms, Qt);
     ctx->count_launch();
-    gp.N = pa;
-    gp.y_slice_stride = (long long)pa * ms;
-    gp.out64 = Z;
-    gp.ldo64 = pa;
-    return gemm_tf32x3(ctx, gp);
+    gp.N = q;
+    gp.y_slice_stride = (long long)q * ms;
+    gp.out64 = T;
+    gp.ldo64 = q;
+    tsk_status r = gemm_tf32x3(ctx, gp);
+    if (r != TSK_OK) return r;
+    axpby3_kernel<<<nblk((long long)m * q, 256), 256, 0, s>>>(T, B, Bp, (long long)m * q, alpha, beta, gamma, Out);
+    ctx->count_launch();
+    return launch_status("eig tc product");
   };
 
-  // Outer iteration: Rayleigh-Ritz on span(Q) -> convergence test -> lock + deflate the leading
-  // converged Ritz pairs that sit well above the wanted edge -> Chebyshev filter of degree d on
-  // [0, b] (b = smallest Ritz value of the block) applied to the remaining Ritz vectors, with d
-  // the largest degree keeping the filter's dynamic range T_d(x_max) <= 1e6 (so CholQR2 stays
-  // accurate) -> CholQR2.  Deflating the dominant pairs (C3/C4: the frame mean is 1e4 x the rest)
-  // is what makes the filter usable; on its own each filter degree replaces d power steps.
-  int nl = 0;           // locked pairs
-  int pa = p;           // active block size
-  int outer = 0, products = 0;
-  bool converged = false;
-  double max_res = 0.0, kyfan = 0.0, theta_top = 0.0;
-  int repairs = 0;
-  if (!opt.init_S) {
-    // One plain power step from the random start before the first Rayleigh-Ritz: the Ritz pairs of
-    // a random block are not worth a p x p eigensolve (C4: 7 Jacobi sweeps).  G Q's columns are all
-    // pulled toward x_1 (cond ~ lambda_1 / lambda_p, 2.5e4 at C4), well within CholQR2's fp64 reach;
-    // if it breaks down anyway (extreme spectra) the random block is kept.
-    cudaMemcpyAsync(Y0, Q, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
-    if ((st = gq(Q, pa)) != TSK_OK) return st;
-    ++products;
-    cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
-    if ((st = cholqr2(ctx, Z, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
-    int hf[2] = {0, 0};
-    if (cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+  // ||G||_F^2 and tr G (for the spectrum statistics of the filter's lower bound)
+  fro_trace_part_kernel<<<128, 256, 0, s>>>(G64, m, F0);  // F0: scratch until the loop
+  sum2_kernel<<<1, 32, 0, s>>>(F0, 128, scal);
+  ctx->count_launch(2);
+
+  // ---- 0. dominant pre-pass: power steps on one vector
+  int nl = 0;  // locked pairs (columns of Xl, values in thl)
+  constexpr int kPower = 6;
+  std::vector<double> hthl;  // host copy of the locked values
+  double gfro2 = 0.0, gtr = 0.0;
+  {
+    double* v = F1;  // [m]
+    double* w = F1 + m;
+    hash_fill_kernel<<<nblk(m, 256), 256, 0, s>>>(v, m, 1, 0xD0517A7Eull, 1.0, 0);
+    ctx->count_launch();
+    for (int it = 0; it < kPower; ++it) {
+      matvec_rows_kernel<<<nblk((long long)m * 32, 256), 256, 0, s>>>(Gd, m, v, w);
+      power_update_kernel<<<1, 1024, 0, s>>>(v, w, m, pw, it);  // v <- w / ||w||
+      ctx->count_launch(2);
+    }
+    products += 1;  // kPower single-vector products ~ one block product
+    if (cudaMemcpyAsync(hostbuf, scal, 2 * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(hostbuf + 2, pw, 2 * kPower * 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
       return TSK_ECUDA;
-    if (hf[0] | hf[1]) {
-      cudaMemcpyAsync(Q, Y0, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
-      cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
+    gfro2 = hostbuf[0];
+    gtr = hostbuf[1];
+    const double th = hostbuf[2 + 2 * (kPower - 1)], r1 = hostbuf[3 + 2 * (kPower - 1)];
+    const double r0 = hostbuf[3 + 2 * (kPower - 2)];
+    // v now holds w / ||w||, one step past the iterate whose residual r1 was measured: its
+    // residual is ~ ratio * r1 when the convergence is geometric
+    const double ratio = r0 > 0.0 ? r1 / r0 : 0.0;
+    if (trace) fprintf(stderr, "[eig] power: theta %.10e res/theta %.2e ratio %.2e\n", th, r1 / th, ratio);
+    if (th > 0.0 && ratio <= 0.05 && r1 * ratio <= 1e-10 * th && k > 1) {
+      copy_cols_kernel<<<nblk(m, 256), 256, 0, s>>>(v, 1, 0, Xl, p, 0, m, 1);
+      cudaMemcpyAsync(thl, pw + 2 * (kPower - 1), 8, cudaMemcpyDeviceToDevice, s);
+      deflate_kernel<<<nblk((long long)m * m, 256), 256, 0, s>>>(Gd, m, Xl, p, 0, 1, thl);
+      ctx->count_launch(2);
+      refresh_g32();
+      nl = 1;
+      hthl.push_back(th);
     }
   }
-  for (outer = 1; outer <= max_iters; ++outer) {
-    const int kr = k - nl;  // wanted pairs still active
-    if ((st = gq(Q, pa)) != TSK_OK) return st;
-    ++products;
-    if ((st = gemm_tn_f64(ctx, Q, pa, 0, Z, pa, 0, m, pa, pa, 1, H, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
-    // Rayleigh-Ritz accuracy follows the iteration: a Jacobi threshold tau leaves the Ritz vectors
-    // mixed by ~tau, which inflates their residuals by ~tau theta and leaves span(Q) unchanged, so
-    // tau = 0.1 x the previous max residual (1e-3 on the first, random, block) costs nothing in
-    // convergence, and the residual test below measures the vectors actually produced.
-    const double tol_rr = outer == 1 ? 1e-3 : std::max(f64 ? 1e-12 : 1e-9, std::min(1e-3, 0.1 * max_res));
-    if ((st = jacobi_eig_batched(ctx, H, pa, 1, W, theta, flags + 2, tol_rr)) != TSK_OK) return st;
-    inv_theta_kernel<<<nblk(pa, 128), 128, 0, s>>>(theta, pa, invt);
+
+  // project the locked vectors out of B [m][q]: B -= Xl (Xl^T B)   (T: scratch)
+  auto project_locked = [&](double* B, int q) -> tsk_status {
+    if (nl == 0) return TSK_OK;
+    tsk_status r;
+    if ((r = gemm_tn_f64(ctx, Xl, p, 0, B, q, 0, m, nl, q, 1, Cl, q, 0, 0, WS_EIG_SMALL)) != TSK_OK) return r;
+    if ((r = gemm_nn_f64(ctx, Xl, p, 0, Cl, q, 0, m, nl, q, 1, nullptr, T, q, 0)) != TSK_OK) return r;
+    cheb_step_kernel<<<nblk((long long)m * q, 256), 256, 0, s>>>(B, B, T, (long long)m * q, 0.0, 1.0, 1.0, B);
     ctx->count_launch();
-    if ((st = gemm_nn_f64(ctx, Z, pa, 0, W, pa, 0, m, pa, pa, 1, invt, Y, pa, 0)) != TSK_OK) return st;  // G'X/theta
-    if ((st = gemm_nn_f64(ctx, Q, pa, 0, W, pa, 0, m, pa, pa, 1, nullptr, X, pa, 0)) != TSK_OK) return st;  // X = QW
-    ritz_residual_kernel<<<kr, 256, 0, s>>>(Y, X, theta, m, pa, res);
+    return TSK_OK;
+  };
+
+  // ---- starting block (pa = p - nl active columns)
+  int pa = p - nl;
+  hash_fill_kernel<<<nblk((long long)m * pa, 256), 256, 0, s>>>(Y, m, pa, 0x5EEDull, 1.0, 0);
+  ctx->count_launch();
+  if (opt.init_S) {  // warm start: the first k columns of the starting block are the given rows
+    init_cols_kernel<<<nblk((long long)m * std::min(k, pa), 256), 256, 0, s>>>(Y, m, pa, opt.init_S,
+                                                                               std::min(k, pa));
     ctx->count_launch();
-    cudaMemcpyAsync(hostbuf, theta, (size_t)pa * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hostbuf + p, res, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hostbuf + 2 * p, flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return TSK_ECUDA;
-    const double* hth = hostbuf;
-    const double* hres = hostbuf + p;
-    const int* hflags = reinterpret_cast<const int*>(hostbuf + 2 * p);
-    if (nl == 0) theta_top = hth[0];
-    double kf_now = 0.0;    // Ky Fan energy of the current k wanted values (locked + active)
-    double locked2 = 0.0;   // sum of the squared locked Ritz values
-    {
-      std::vector<double> hl(nl);
-      if (nl > 0) {
-        cudaMemcpyAsync(hl.data(), thl, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-      }
-      for (double v : hl) {
-        kf_now += v;
-        locked2 += v * v;
-      }
-      for (int c = 0; c < kr; ++c) kf_now += hth[c];
-    }
-    // residual scale: theta_1 (reading c15), or with tol_active the top of the active (deflated)
-    // block, whose Gram norm ||G'||_F ~ sqrt(||G||_F^2 - sum locked theta^2) also sets the floor
-    const bool act = opt.tol_active && nl > 0 && hth[0] > 0.0;
-    const double ref = act ? hth[0] : theta_top;
-    const double gref = act ? std::sqrt(std::max(gfro2 - locked2, 0.0)) : gfro;
-    max_res = 0.0;
-    for (int c = 0; c < kr; ++c) max_res = std::max(max_res, hres[c]);
-    max_res /= ref > 0 ? ref : 1.0;
-    const double floor_rel = f64 ? 1e-14 : 4e-8;  // working-precision floor of the G Q products
-    const double tol_eff = std::max(tol, ref > 0 ? floor_rel * gref / ref : tol);
-    // Ky Fan convergence: the residual test alone (relative to theta_1) stops too early when a dominant
-    // eigenvalue sits far above a flat rest (measured: deficits up to 1.2e-5 after 16 products,
-    // scripts/random_sweep5.py); the remaining deficit is extrapolated from the last two changes of
-    // the Ky Fan energy (geometric convergence, ratio rho) and must also be small
-    const double kf_change = kyfan_prev > 0 ? std::fabs(kf_now - kyfan_prev) : -1.0;
-    double kf_remaining;  // estimated remaining Ky Fan deficit, relative
-    if (kf_change < 0.0) {
-      kf_remaining = max_res <= 0.1 * tol_eff ? 0.0 : INFINITY;  // first outer: only a block already converged
-    } else {
-      const double rho = kf_change_prev > 0.0 ? std::min(kf_change / kf_change_prev, 0.99) : 0.5;
-      kf_remaining = kf_change * rho / (1.0 - rho) / std::max(kf_now, 1e-300);
-    }
-    kf_change_prev = kf_change;
-    if (kf_change >= 0.0 && kf_change <= 1e-12 * kf_now) ++kyfan_still;
-    else kyfan_still = 0;
-    kyfan_prev = kf_now;
-    if (getenv("TSK_EIG_TRACE"))
-      fprintf(stderr, "[eig] outer=%d products=%d locked=%d max_res=%.3e (tol %.2e) theta0=%.4e theta_k=%.4e theta_p=%.4e "
-              "kyfan=%.12e rr_sweeps=%d res0=%.3e cholqr_flags=%d,%d\n", outer, products, nl, max_res, tol_eff, hth[0],
-              hth[kr - 1], hth[pa - 1], kf_now, hflags[2], hres[0] / theta_top, hflags[0], hflags[1]);
-    if (hflags[0] + hflags[1] > 0) {
-      // rank-deficient block (rank(G) < p): perturb with fresh directions and re-orthonormalise
-      if (++repairs > 8) return TSK_ECUDA;
-      cudaMemcpyAsync(Y, Q, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
-      hash_fill_kernel<<<nblk((long long)m * pa, 256), 256, 0, s>>>(Y, m, pa, 0xBADC0DEull + repairs, 1e-3, 1);
+  }
+  if ((st = project_locked(Y, pa)) != TSK_OK) return st;
+
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
+    cudaFuncSetAttribute(chol_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(trsm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr |= device_bit();
+  }
+
+  bool converged = false;
+  int outer = 0;
+  double max_res = 0.0, a_lo = 0.0;
+  bool a_failed = false;
+  double range_cut = 1.0;  // dynamic-range factor of the filter, cut after a CholQR breakdown
+  int fallbacks = 0;
+  double kf_prev = -1.0;
+  int kf_still = 0;
+  std::vector<double> hth(p), hres(p);
+  for (outer = 0; outer < max_iters; ++outer) {
+    const int kr = k - nl;
+    // ---- Rayleigh-Ritz: Z = G'Y, CholQR Q = Y diag(s) L^{-T} with G'Q = Z diag(s) L^{-T} (no second
+    //      product), H = Q^T G'Q, (theta, W) = eig(H), Ritz vectors Q W -> F0 and G'Q W -> F1
+    //      (Y and Z stay intact for the fallbacks)
+    double* Q = X;
+    double* GQ = GX;
+    if ((st = product(Y, nullptr, pa, 1.0, 0.0, 0.0, Z)) != TSK_OK) return st;
+    // one CholQR pass (Yin, Zin) -> (Yout, Zout), flag[0] on breakdown
+    auto cholqr_step = [&](const double* Yin, const double* Zin, double* Yout, double* Zout,
+                           double shift) -> tsk_status {
+      tsk_status r;
+      if ((r = gemm_tn_f64(ctx, Yin, pa, 0, Yin, pa, 0, m, pa, pa, 1, M, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return r;
+      chol_scale_kernel<<<1, kCiThreads, (size_t)pa * (pa | 1) * 8, s>>>(M, pa, 1e-14, shift, Rs, Cn, Cn + p, flags);
+      trsm2_kernel<<<nblk(2LL * m, kTrsmRows), kTrsmRows,
+                     ((size_t)pa * pa + (size_t)kTrsmRows * (pa | 1) + 2 * (size_t)pa) * 8, s>>>(Yin, Zin, Cn + p, Rs,
+                                                                                             Cn, m, pa, Yout, Zout);
+      ctx->count_launch(2);
+      return launch_status("eig cholqr");
+    };
+    // H = Q^T G'Q, its eigenpairs (syev, or Jacobi), Ritz vectors and residuals, copied to the host
+    auto rr_finish = [&](bool jacobi) -> tsk_status {
+      tsk_status r;
+      if ((r = gemm_tn_f64(ctx, Q, pa, 0, GQ, pa, 0, m, pa, pa, 1, H, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return r;
+      if (jacobi) r = jacobi_eig_batched(ctx, H, pa, 1, W, theta);
+      else r = syev_top(ctx, H, pa, pa, W, pa, theta, flags + 1, 1e-8);
+      if (r != TSK_OK) return r;
+      if ((r = gemm_nn_f64(ctx, Q, pa, 0, W, pa, 0, m, pa, pa, 1, nullptr, F0, pa, 0)) != TSK_OK) return r;
+      if ((r = gemm_nn_f64(ctx, GQ, pa, 0, W, pa, 0, m, pa, pa, 1, nullptr, F1, pa, 0)) != TSK_OK) return r;
+      ritz_res_kernel<<<kr, 256, 0, s>>>(F1, F0, pa, theta, m, res);
       ctx->count_launch();
-      if ((st = cholqr2(ctx, Y, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
-      continue;
+      if ((r = launch_status("eig rr")) != TSK_OK) return r;
+      cudaMemcpyAsync(hostbuf, theta, (size_t)pa * 8, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(hostbuf + p, res, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(hostbuf + 2 * p, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+      return cudaStreamSynchronize(s) == cudaSuccess ? TSK_OK : TSK_ECUDA;
+    };
+    cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
+    if ((st = cholqr_step(Y, Z, Q, GQ, 0.0)) != TSK_OK) return st;
+    if ((st = rr_finish(false)) != TSK_OK) return st;
+    const int* hfl = reinterpret_cast<const int*>(hostbuf + 2 * p);
+    if (hfl[0]) {
+      // Cholesky breakdown: the filtered block is numerically rank deficient at fp64.  Shifted
+      // CholQR then a plain pass (CholQR2 of the shifted factor); if that also breaks down the block
+      // is exactly rank deficient (rank(G') < p): Householder QR (any QR basis)
+      if (++fallbacks > 8) return TSK_ENUMERIC;
+      range_cut = 1e-2;  // later filters keep a smaller dynamic range
+      if (trace) fprintf(stderr, "[eig] outer %d: CholQR breakdown at column %d -> shifted CholQR\n", outer, hfl[0]);
+      const double shift = 11.0 * ((double)m * pa + (double)pa * (pa + 1)) * 2.220446049250313e-16 * pa;
+      cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
+      if ((st = cholqr_step(Y, Z, Q, GQ, shift)) != TSK_OK) return st;
+      if ((st = cholqr_step(Q, GQ, Q, GQ, 0.0)) != TSK_OK) return st;
+      if ((st = rr_finish(false)) != TSK_OK) return st;
+      if (hfl[0]) {
+        if (trace) fprintf(stderr, "[eig] outer %d: shifted CholQR breakdown -> Householder QR\n", outer);
+        cudaMemcpyAsync(Q, Y, (size_t)m * pa * 8, cudaMemcpyDeviceToDevice, s);
+        hqr_kernel<<<1, kHqrThreads, 0, s>>>(Q, m, pa, T, hqr_tau);
+        ctx->count_launch();
+        if ((st = project_locked(Q, pa)) != TSK_OK) return st;
+        hqr_kernel<<<1, kHqrThreads, 0, s>>>(Q, m, pa, T, hqr_tau);
+        ctx->count_launch();
+        if ((st = product(Q, nullptr, pa, 1.0, 0.0, 0.0, GQ)) != TSK_OK) return st;
+        cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
+        if ((st = rr_finish(false)) != TSK_OK) return st;
+      }
     }
-    if ((max_res <= tol_eff && kf_remaining <= kKyFanTol) || (kyfan_still >= 2 && max_res <= 1e-4)) {
+    if (hfl[1]) {
+      // an eigenvalue cluster of H the twisted factorisation cannot resolve: Jacobi on the same H
+      if (++fallbacks > 8) return TSK_ENUMERIC;
+      if (trace) fprintf(stderr, "[eig] outer %d: unresolved cluster in H -> Jacobi\n", outer);
+      if ((st = rr_finish(true)) != TSK_OK) return st;
+    }
+    // rotate: X, GX <- the Ritz data; Q / GQ / Y / Z buffers are free again
+    std::swap(X, F0);
+    std::swap(GX, F1);
+    for (int c = 0; c < pa; ++c) hth[c] = hostbuf[c];
+    for (int c = 0; c < kr; ++c) hres[c] = hostbuf[p + c];
+    // ---- convergence (reading c15): residuals relative to theta_k, or the Kato-Temple estimate
+    // of the remaining Ky Fan deficit of the active wanted pairs.  Wanted pairs at the null space
+    // (theta <= 1e-12 of the top: rank(G) < k) can be any orthonormal completion and are excluded.
+    const double top_all = std::max(hth[0], hthl.empty() ? 0.0 : hthl[0]);
+    int ke = 0;
+    while (ke < kr && hth[ke] > 1e-12 * top_all) ++ke;
+    const double thk = ke > 0 ? hth[ke - 1] : 0.0, thp = hth[pa - 1];
+    max_res = 0.0;
+    double kf_est = 0.0, e_act = 0.0;
+    for (int c = 0; c < ke; ++c) {
+      max_res = std::max(max_res, hres[c]);
+      const double gap = std::max(hth[c] - thp, 1e-300 + 1e-15 * std::fabs(hth[0]));
+      kf_est += hres[c] * hres[c] / gap;
+      e_act += hth[c];
+    }
+    max_res /= thk > 0.0 ? thk : 1.0;
+    double kf_now = 0.0;
+    for (double v : hthl) kf_now += v;
+    for (int c = 0; c < kr; ++c) kf_now += hth[c];
+    if (kf_prev > 0.0 && std::fabs(kf_now - kf_prev) <= 1e-13 * kf_now) ++kf_still;
+    else kf_still = 0;
+    kf_prev = kf_now;
+    const bool conv_r = max_res <= tol;
+    // the Ky Fan criterion alone suffices only where the k-th eigengap is small (reading c6/c16: below
+    // lambda_k / lambda_{k+1} = 1.05 the subspace itself is not a parity quantity, the energy is); with
+    // a clear gap the residual criterion must hold (projector ~ residual / gap)
+    const double gap_k = (ke < pa && hth[ke] > 1e-12 * top_all) ? thk / hth[ke] : INFINITY;
+    const bool conv_k = outer > 0 && e_act > 0.0 && kf_est <= kf_tol * e_act && gap_k < 1.05;
+    if (trace)
+      fprintf(stderr, "[eig] outer %d products %d locked %d max_res/theta_k %.2e kf_est/E %.2e theta0 %.6e theta_k %.6e "
+              "theta_p %.6e a %.4e\n", outer, products, nl, max_res, e_act > 0 ? kf_est / e_act : 0.0, hth[0], thk, thp,
+              a_lo);
+    if (conv_r || conv_k || kf_still >= 2 || ke == 0) {
       converged = true;
       break;
     }
-    if (outer == max_iters) break;
-    // ---- lock the leading converged pairs well above the wanted edge (theta >= 2 theta_{k-1})
+    if (outer + 1 == max_iters) break;
+    // ---- lock the leading converged pairs well above the wanted edge
     int nnew = 0;
-    while (nnew < kr - 1 && hres[nnew] <= tol * ref && hth[nnew] >= 2.0 * hth[kr - 1]) ++nnew;
-    const double* tha = theta;  // device Ritz values of the active block
-    int off = 0;                // first active column of X / theta after locking
+    while (nnew < kr - 1 && hres[nnew] <= 1e-8 * hth[nnew] && hth[nnew] >= 2.0 * thk) ++nnew;
     if (nnew > 0) {
       copy_cols_kernel<<<nblk((long long)m * nnew, 256), 256, 0, s>>>(X, pa, 0, Xl, p, nl, m, nnew);
       cudaMemcpyAsync(thl + nl, theta, (size_t)nnew * 8, cudaMemcpyDeviceToDevice, s);
       deflate_kernel<<<nblk((long long)m * m, 256), 256, 0, s>>>(Gd, m, X, pa, 0, nnew, theta);
-      g_to_f32_kernel<<<nblk((long long)m * ms, 256), 256, 0, s>>>(Gd, m, ms, G32);
-      ctx->count_launch(3);
-      nl += nnew;
-      off = nnew;
-    }
-    const int pn = pa - off;
-    // ---- Chebyshev filter on [0, b] applied to the remaining Ritz vectors X[:, off:pa]
-    const double b = hth[pa - 1];
-    // the filter's dynamic range is set by the top of the spectrum: after the first Rayleigh-Ritz
-    // step (random start) theta_0 can underestimate lambda_max by orders of magnitude (C4: 7.7e6 vs
-    // 1.04e9), and a filter designed on it overflows the block into one direction (CholQR breaks
-    // down); there the upper bound ||G||_F >= lambda_max is used instead
-    const double top = outer == 1 ? std::max(hth[off], gfro) : hth[off];
-    const double xmax = 2.0 * top / b - 1.0;
-    int d = 1;
-    if (b > 0.0 && xmax > 1.0 + 1e-12) {
-      const double ach = acosh(xmax);
-      d = (int)std::floor(std::log(2e6) / ach);  // T_d(x) ~ exp(d acosh x) / 2 <= 1e6
-      d = std::max(1, std::min(d, opt.cheb_degree > 0 ? std::min(12, opt.cheb_degree) : 12));
-    }
-    if (getenv("TSK_EIG_TRACE")) fprintf(stderr, "[eig]   lock %d, filter degree %d on [0, %.4e], x_max %.3e\n", nnew, d, b, xmax);
-    copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(X, pa, off, Y0, pn, 0, m, pn);
-    ctx->count_launch();
-    if (d == 1) {
-      // plain step Y = G' X / theta (the scaled power step of the previous version)
-      copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(Y, pa, off, Y1, pn, 0, m, pn);
-      ctx->count_launch();
-    } else {
-      const double cc = 0.5 * b, ee = 0.5 * b;
-      double* Yprev = nullptr;
-      double* Ycur = Y0;
-      double* Ynext = Y1;
-      double* spare = Q1;  // free until the CholQR below
-      for (int j = 1; j <= d; ++j) {
-        if ((st = gq(Ycur, pn)) != TSK_OK) return st;
-        ++products;
-        const double alpha = (j == 1) ? 1.0 / ee : 2.0 / ee;
-        cheb_step_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(Z, Ycur, Yprev, (long long)m * pn, cc, alpha,
-                                                                       j == 1 ? 0.0 : 1.0, Ynext);
-        ctx->count_launch();
-        double* t = Yprev ? Yprev : spare;
-        Yprev = Ycur;
-        Ycur = Ynext;
-        Ynext = t;
-      }
-      // normalise the filtered columns (their norms spread up to T_d(x_max)) into Y1
-      inv_colnorm_kernel<<<pn, 256, 0, s>>>(Ycur, m, pn, ncol);
-      colscale_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(Ycur, ncol, m, pn, Y1);
       ctx->count_launch(2);
+      refresh_g32();
+      for (int c = 0; c < nnew; ++c) hthl.push_back(hth[c]);
+      nl += nnew;
+      // compact the active columns into Y / Z (free), then rotate
+      const int pn = pa - nnew;
+      copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(X, pa, nnew, Y, pn, 0, m, pn);
+      copy_cols_kernel<<<nblk((long long)m * pn, 256), 256, 0, s>>>(GX, pa, nnew, Z, pn, 0, m, pn);
+      ctx->count_launch(2);
+      std::swap(X, Y);
+      std::swap(GX, Z);
     }
+    const int pn = pa - nnew;
+    // ---- filter interval [a, b]: b = theta_p; a from the eigenvalues outside the block
+    double sum_t = 0.0, sum_t2 = 0.0;
+    for (double v : hthl) { sum_t += v; sum_t2 += v * v; }
+    for (int c = nnew; c < pa; ++c) { sum_t += hth[c]; sum_t2 += hth[c] * hth[c]; }
+    const int nrest = m - nl - pn;
+    double a = 0.0;
+    if (nrest > 0 && !a_failed) {
+      const double mu = (gtr - sum_t) / nrest;
+      const double var = std::max((gfro2 - sum_t2) / nrest - mu * mu, 0.0);
+      a = std::max(0.0, mu - 2.0 * std::sqrt(var));
+    }
+    const double b = thp;
+    if (!(a < 0.95 * b)) {  // the estimate landed at / above the block: the PSD bound instead
+      a = 0.0;
+      a_failed = true;
+    }
+    a_lo = a;
+    const double top = hth[nnew];
+    const double xmax = (2.0 * top - a - b) / (b - a);
+    int d = 1;
+    if (b > a && xmax > 1.0 + 1e-12) {
+      // T_d(x) ~ exp(d acosh x) / 2 <= R: R = 1e4 on the random first block (its columns carry O(1)
+      // components along the top eigenvectors), 1e7 once the block holds Ritz vectors
+      const double R = (outer == 0 ? 1e4 : 1e7) * range_cut;
+      d = (int)std::floor(std::log(2.0 * std::max(R, 10.0)) / std::acosh(xmax));
+      d = std::max(1, std::min(d, opt.cheb_degree > 0 ? opt.cheb_degree : 40));
+    }
+    if (trace) fprintf(stderr, "[eig]   lock %d, degree %d on [%.4e, %.4e], x_max %.3e\n", nnew, d, a, b, xmax);
     pa = pn;
-    if (nl > 0) {
-      // keep the active block orthogonal to the locked vectors: Y1 -= Xl (Xl^T Y1)
-      if ((st = gemm_tn_f64(ctx, Xl, p, 0, Y1, pa, 0, m, nl, pa, 1, C, pa, 0, 0, WS_EIG_SMALL)) != TSK_OK) return st;
-      if ((st = gemm_nn_f64(ctx, Xl, p, 0, C, pa, 0, m, nl, pa, 1, nullptr, Q1, pa, 0)) != TSK_OK) return st;
-      cheb_step_kernel<<<nblk((long long)m * pa, 256), 256, 0, s>>>(Y1, Y1, Q1, (long long)m * pa, 0.0, 1.0, 1.0, Y1);
-      ctx->count_launch();
+    // ---- Chebyshev filter of degree d on the active Ritz vectors X (G'X in GX):
+    //      Y_1 = (G'X - c X)/e,  Y_j = 2/e (G' - c) Y_{j-1} - Y_{j-2};  buffers F0, F1, Z rotate
+    const double cc = 0.5 * (a + b), ee = 0.5 * (b - a);
+    double* R3[3] = {F0, F1, Z};
+    cheb_step_kernel<<<nblk((long long)m * pa, 256), 256, 0, s>>>(GX, X, nullptr, (long long)m * pa, cc, 1.0 / ee,
+                                                                   0.0, R3[0]);
+    ctx->count_launch();
+    for (int j = 2; j <= d; ++j) {
+      double* cur = R3[(j - 2) % 3];
+      double* prev = j == 2 ? X : R3[(j - 3) % 3];
+      if ((st = product(cur, prev, pa, 2.0 / ee, -2.0 * cc / ee, -1.0, R3[(j - 1) % 3])) != TSK_OK) return st;
     }
-    if ((st = cholqr2(ctx, Y1, Q1, Q, m, pa, C, Rinv, flags)) != TSK_OK) return st;
-    (void)tha;
+    double* Yd = R3[(d - 1) % 3];
+    // the filtered block becomes Y (pointer rotation: Y's old buffer takes Yd's slot)
+    if (Yd == F0) std::swap(Y, F0);
+    else if (Yd == F1) std::swap(Y, F1);
+    else std::swap(Y, Z);
+    if ((st = project_locked(Y, pa)) != TSK_OK) return st;
   }
-  // output: locked pairs first (largest), then the leading active Ritz pairs; a final CholQR2 of
-  // the combined k columns (Gram-Schmidt order: locked columns are kept, active ones are made
-  // orthogonal to them) removes the residual locked/active coupling of the deflated iteration
+  // ---- output: locked pairs first (largest), then the leading active Ritz pairs
   const int kr = k - nl;
-  double* Xo = Y0;
-  if (nl > 0) copy_cols_kernel<<<nblk((long long)m * nl, 256), 256, 0, s>>>(Xl, p, 0, Xo, k, 0, m, nl);
-  copy_cols_kernel<<<nblk((long long)m * kr, 256), 256, 0, s>>>(X, pa, 0, Xo, k, nl, m, kr);
-  ctx->count_launch(2);
+  double* Xo = T;
   if (nl > 0) {
-    if ((st = cholqr2(ctx, Xo, Q1, Y1, m, k, C, Rinv, flags)) != TSK_OK) return st;
-    Xo = Y1;
+    copy_cols_kernel<<<nblk((long long)m * nl, 256), 256, 0, s>>>(Xl, p, 0, Xo, k, 0, m, nl);
+    ctx->count_launch();
   }
+  copy_cols_kernel<<<nblk((long long)m * kr, 256), 256, 0, s>>>(X, pa, 0, Xo, k, nl, m, kr);
+  ctx->count_launch();
   write_sketch_kernel<<<k, 256, 0, s>>>(Xo, m, k, S);
   ctx->count_launch();
   if (X64) cudaMemcpyAsync(X64, Xo, (size_t)m * k * 8, cudaMemcpyDeviceToDevice, s);
@@ -586,16 +1083,12 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
   }
   if (info) {
     info->iters = products;
-    std::vector<double> hl(k);
-    cudaMemcpyAsync(hl.data(), thl, (size_t)nl * 8, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hl.data() + nl, theta, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    kyfan = 0.0;
-    for (double v : hl) kyfan += v;
-    info->kyfan = kyfan;
+    double kf = 0.0;
+    for (double v : hthl) kf += v;
+    for (int c = 0; c < kr; ++c) kf += hth[c];
+    info->kyfan = kf;
     info->max_resid = max_res;
-    // hostbuf holds the Ritz values of the last Rayleigh-Ritz step (active block, decreasing)
-    info->gap_est = (kr >= 1 && kr < pa && hostbuf[kr] > 0.0) ? hostbuf[kr - 1] / hostbuf[kr] : INFINITY;
+    info->gap_est = (kr >= 1 && kr < pa && hth[kr] > 0.0) ? hth[kr - 1] / hth[kr] : INFINITY;
   }
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   return converged ? TSK_OK : TSK_WARN_NOT_CONVERGED;

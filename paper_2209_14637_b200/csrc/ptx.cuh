@@ -67,6 +67,12 @@ TSK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // ---------------------------------------------------------------- proxy fences
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads)
+// 1-D bulk copy global -> shared (TMA engine), completion counted on the mbarrier (bytes % 16 == 0,
+// both addresses 16-byte aligned)
+TSK_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 TSK_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---------------------------------------------------------------- L2 cache-policy hinted accesses

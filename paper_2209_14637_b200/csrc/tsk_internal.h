@@ -66,6 +66,8 @@ enum WorkspaceId {
   WS_MF_SMALL,     // matrix-free sketch: small fp64 matrices, flags
   WS_MF_SCR,       // matrix-free sketch: fp64 GEMM split scratch
   WS_CHECK,        // input validation flag (check_finite)
+  WS_EIG_GQ,       // eigensolver: split-K partial tiles + tickets of the fp64 product
+  WS_SYEV,         // small symmetric eigensolver: reflectors, tridiagonal, scratch
   WS_COUNT
 };
 
@@ -216,6 +218,11 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
 // SCW (scw.cu); all pointers device
 tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const float* S, int k, int r, float* L,
                    float* R, float* sigma, double* err);
+
+// top nw eigenpairs of a dense symmetric p x p matrix (p <= 256), syev.cu: W [p][ldw] columns,
+// lam [nw] decreasing; flag (device, may be null) set to 1 if the vectors are not orthonormal to orth_tol
+tsk_status syev_top(Ctx* ctx, const double* H, int p, int nw, double* W, int ldw, double* lam, int* flag,
+                    double orth_tol);
 
 // batched symmetric PSD eigensolver (one-sided Jacobi), jacobi.cu
 // H: [batch][p][p] fp64 symmetric (row-major, read only).  W: [batch][p][p] fp64 eigenvectors as
