@@ -731,7 +731,7 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     return topk_dense(ctx, G64, m, k, S, lambda, info, X64);
   }
   if (p > 128) return TSK_EINVAL;
-  const bool tc = !f64_products && m > 2048 && !getenv("TSK_EIG_F64");
+  const bool tc = !f64_products && (m > 2048 || getenv("TSK_EIG_TC")) && !getenv("TSK_EIG_F64");
   cudaStream_t s = ctx->stream;
   tsk_status st;
 
@@ -1029,10 +1029,11 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       a = std::max(0.0, mu - 2.0 * std::sqrt(var));
     }
     const double b = thp;
-    if (!(a < 0.95 * b)) {  // the estimate landed at / above the block: the PSD bound instead
-      a = 0.0;
-      a_failed = true;
-    }
+    // the estimate must sit below the block (a flat spectrum puts it close: C5 has a / b ~ 0.92); a
+    // block whose smallest Ritz value fell below the previous a shows the estimate was too high
+    // (eigenvalues under a are amplified by the filter): the PSD bound a = 0 from then on
+    if (outer > 0 && thp < a_lo) a_failed = true;
+    if (a_failed || !(a < b * (1.0 - 1e-3))) a = 0.0;
     a_lo = a;
     const double top = hth[nnew];
     const double xmax = (2.0 * top - a - b) / (b - a);

@@ -48,8 +48,12 @@ def test_c4_full_size_path():
     lamg = lam.cpu().numpy()
     assert np.linalg.norm(Sd @ Sd.T - np.eye(c.k)) <= 1e-5
     assert abs(tucker1.kyfan_energy(Gg, Sd) - w[: c.k].sum()) <= 1e-6 * w[: c.k].sum()
-    # Ritz values to the precision of the 3xTF32 G Q products, relative to the top of the spectrum
-    assert np.max(np.abs(lamg - w[: c.k])) <= 1e-6 * w[0]
+    # the k - 1 directions below the dominant frame mean on their own scale (DESIGN reading c15: the
+    # stopping rule measures residuals against theta_k, not theta_1)
+    assert w[0] >= 20 * w[1]
+    assert abs(tucker1.kyfan_energy(Gg, Sd) - w[: c.k].sum()) <= 1e-6 * w[1: c.k].sum()
+    # Ritz values (fp64 products) relative to the k-th eigenvalue, not the dominant one
+    assert np.max(np.abs(lamg - w[: c.k])) <= 1e-6 * w[c.k - 1]
     res = np.linalg.norm(Gg @ Sd.T - Sd.T * (np.einsum("ij,jk,ik->i", Sd, Gg, Sd))[None, :], axis=0)
     assert np.max(res) <= 1e-5 * w[0]
     big = np.argmax(np.abs(Sd), axis=1)
