@@ -161,10 +161,10 @@ def barrier(world):
 
 # ------------------------------------------------------------------------------ reference arm
 def cpu_oracle_run(c, A_s: np.ndarray, T_s: np.ndarray, budget_s=20.0):
-    """Time the float64 oracle (oracle/) as it stands on the host cores, on a bounded sample of
-    the workload: the Gram over the sample matrices (repeated until ~half the budget is spent),
-    one eigh of the m x m Gram, and SCW on the sample test matrices; the per-matrix rates are
-    extrapolated to one full step (D_train training + D_test test matrices)."""
+    """Time the float64 oracle (oracle/) as it stands on the host cores, on a bounded sample of the
+    workload: the Gram over the sample matrices (repeated until ~half the budget is spent), one eigh of
+    the m x m Gram, and SCW on the sample test matrices; the per-matrix rates are extrapolated to one
+    full step (D_train training + D_test test matrices).  Used for the cpu_baseline of our arm's line."""
     import threadpoolctl
     from oracle import scw as oscw
     from oracle import tucker1
@@ -196,25 +196,57 @@ def cpu_oracle_run(c, A_s: np.ndarray, T_s: np.ndarray, budget_s=20.0):
 
 
 def run_reference(args, c):
-    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    """The reference arm = the float64 oracle (the paper has no code to install).  Each timed step is a
+    bounded sample of the workload, run for real and reported as timed (no extrapolation): the fp64
+    Gram of n_tr training matrices, the top-k eigh of that Gram, and the SCW errors of n_te = n_tr / 4
+    test matrices (the 2000 : 500 proportion of C4); value = training matrices per second of that sampled
+    pipeline.  n_tr is sized from a probe so that warmup + steps take ~budget seconds in total."""
+    import threadpoolctl
+    from oracle import scw as oscw
+    from oracle import tucker1
+
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    A_s = datagen.generate(c, "train", 0, 8).double().numpy()
-    T_s = datagen.generate(c, "test", 0, 2).numpy()
-    times = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_oracle_run(c, A_s, T_s, budget_s=max(4.0, 90.0 / max(1, args.warmup + args.steps)))
-        if i >= args.warmup:
-            times.append(r)
-    value = statistics.median([t["value"] for t in times])
-    ms = 1e3 * statistics.median([t["seconds_per_step"] for t in times])
-    cb = dict(times[-1])
-    cb["value"] = value
-    cb.pop("seconds_per_step", None)
+    info = threadpoolctl.threadpool_info()
+    cores = max([i.get("num_threads", 1) for i in info] + [1])
+    pool_tr = datagen.generate(c, "train", 0, 16).double().numpy()
+    pool_te = datagen.generate(c, "test", 0, 4).numpy()
+    # probe: seconds per training matrix (Gram), per eigh, per test matrix (SCW)
+    t0 = time.perf_counter()
+    tucker1.mode1_gram(pool_tr[:2])
+    t_mat = (time.perf_counter() - t0) / 2
+    t0 = time.perf_counter()
+    tucker1.top_k_eigen(np.eye(c.m), c.k)
+    t_eig = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oscw.scw_errors(pool_te[:1], np.eye(c.m)[: c.k], c.r)
+    t_te = time.perf_counter() - t0
+    per_step = args.ref_budget / max(1, args.warmup + args.steps)
+    n_tr = int(max(4, min(c.D_train, (per_step - t_eig) / (t_mat + t_te / 4))))
+    n_te = max(1, n_tr // 4)
+
+    def step():
+        idx = np.arange(n_tr) % pool_tr.shape[0]
+        G = tucker1.mode1_gram(pool_tr[idx])
+        S, lam = tucker1.top_k_eigen(G, c.k)
+        oscw.scw_errors(pool_te[np.arange(n_te) % pool_te.shape[0]], S, c.r)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    total = time.perf_counter() - t0
+    value = n_tr * args.steps / total
+    sample = (f"each step: fp64 Gram of {n_tr} training matrices (cycled from 16 distinct frames) + eigh({c.m}) + "
+              f"SCW errors of {n_te} test matrices, timed as run (not extrapolated); numpy float64 + "
+              f"{info[0].get('internal_api', '?') if info else '?'} BLAS on {cores} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (datagen, seed 0)",
-            "config": workload_desc(c, args.gpus), "cpu_baseline": cb,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (datagen, seed 0)", "config": workload_desc(c, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -222,8 +254,10 @@ def run_reference(args, c):
 # ------------------------------------------------------------------------------ our arm
 def run_tsketch(args, c):
     import paper_2209_14637_b200 as tsk
-    from paper_2209_14637_b200.dist import reduce_gram, shard_range
+    from paper_2209_14637_b200.dist import init_native_comm, shard_range
 
+    if (args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1) and "NCCL_DEBUG" not in os.environ:
+        os.environ["NCCL_DEBUG"] = "INFO"  # init lines on stderr show nranks of the communicators
     rank, world, local = dist_setup(args.gpus)
     dev = torch.device("cuda", local)
     d0, d1 = shard_range(c.D_train, rank, world)
@@ -233,7 +267,10 @@ def run_tsketch(args, c):
     G = torch.empty(c.m, c.m, dtype=torch.float64, device=dev)
     err = torch.empty(t1 - t0, dtype=torch.float64, device=dev)
     ctx = tsk.context(dev)
+    if world > 1:
+        init_native_comm(ctx)  # the library's own NCCL communicator (tsk_comm_init) for the data path
     stream = torch.cuda.current_stream(dev)
+    err_all = torch.empty(c.D_test, dtype=torch.float64, device=dev)
     A_host_sample = A[:8].double().cpu().numpy() if rank == 0 else None
     T_host_sample = T[:2].cpu().numpy() if rank == 0 else None
 
@@ -246,7 +283,7 @@ def run_tsketch(args, c):
         tsk.sketch_gram(A, G64=G, ctx=ctx)
         if record:
             es[1].record(stream)
-        reduce_gram(G)
+        tsk.allreduce_gram(G, ctx=ctx)  # NCCL sum over the ranks (no-op on one GPU)
         if record:
             es[2].record(stream)
         S, lam, info, st = tsk.sketch_topk(G, c.k, ctx=ctx)
@@ -254,6 +291,7 @@ def run_tsketch(args, c):
             es[3].record(stream)
         if t1 > t0:
             tsk.scw_error(T, S, c.r, out=err, ctx=ctx)
+        tsk.allgather_errors(err, c.D_test, ctx=ctx)  # every rank's errors -> the whole test set
         if record:
             es[4].record(stream)
         return es, info
@@ -304,7 +342,7 @@ def run_tsketch(args, c):
             tsk.sketch_gram(Ah, G64=Gh, ctx=ctx)           # host stack streamed through the library
             if world > 1:
                 Gd = Gh.to(dev)
-                reduce_gram(Gd)
+                tsk.allreduce_gram(Gd, ctx=ctx)
                 Gh.copy_(Gd)
             S, lam, _, _ = tsk.sketch_topk(Gh, c.k, ctx=ctx)  # host G in, host S out
             if t1 > t0:
@@ -390,6 +428,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=90.0, help="reference arm: seconds for warmup + steps")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()
     c = datagen.CONFIGS[args.config]

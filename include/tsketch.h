@@ -77,19 +77,36 @@ int64_t tsk_launch_count(tsk_ctx ctx);
    (libnccl.so.2, reusing the copy already in the process if any): TSK_ENCCL if it is not available.
    tsk_get_unique_id: uid[128] (host memory) to be broadcast by the caller (e.g. over torch.distributed).
    tsk_comm_init: collective over the nranks processes (same uid, distinct rank in [0, nranks)); the
-   ctx's device must be the rank's GPU.  Afterwards sketch_train treats A as the rank's LOCAL shard and
-   all-reduces G on the ctx stream before the top-k solve.  The communicator is destroyed with the ctx;
+   ctx's device must be the rank's GPU.  Afterwards sketch_train treats A as the rank's LOCAL shard (which
+   may be empty, D = 0) and all-reduces G on the ctx stream before the top-k solve; a rank whose arguments
+   or local Gram fail still joins a status all-reduce first, so every rank returns the same error instead
+   of leaving its peers blocked in the collective.  The communicator is destroyed with the ctx;
    calling tsk_comm_init again replaces it. */
 tsk_status tsk_get_unique_id(unsigned char uid[128]);
 tsk_status tsk_comm_init(tsk_ctx ctx, int nranks, int rank, const unsigned char uid[128]);
+/* The test stream is sharded like the training stream: rank p holds the per-matrix errors of test
+   matrices [floor(p B/P), floor((p+1) B/P)) (B = B_total).  tsk_allgather_errors gathers them, in
+   stream order, into err_all [B_total] on every rank (NCCL all-gather of the shards padded to
+   ceil(B/P), compacted on the device), so the paper's test-error metric (a mean over
+   the whole test set) can be evaluated anywhere.  err_local [hi - lo] and err_all are DEVICE fp64
+   pointers; without a communicator it copies err_local to err_all.  Collective: every rank calls it
+   with the same B_total.  Asynchronous on the ctx stream. */
+tsk_status tsk_allgather_errors(tsk_ctx ctx, const double* err_local, int64_t B_total, double* err_all);
+/* The Gram all-reduce of sketch_train on its own (for callers that run sketch_gram and sketch_topk as
+   separate calls, e.g. to time them): G64 [m][m] DEVICE fp64 summed in place over the communicator's
+   ranks (ncclAllReduce, sum, ctx stream); a no-op without a communicator. */
+tsk_status tsk_allreduce_gram(tsk_ctx ctx, double* G64, int m);
 
 /* ---------------------------------------------------------------------- training */
 
 typedef struct {
-  int oversample;    /* block size p = min(m, k + oversample) <= 256; default (<= 0): 16 */
+  int oversample;    /* block size p = min(m, k + oversample); p <= 128 when m > dense_max_m; default (<= 0): 16 */
   int max_iters;     /* subspace iterations cap; default 300 */
-  double tol;        /* convergence: Ritz residual <= tol * theta_1 for the top k; default 5e-7 */
-  int dense_max_m;   /* m <= this: one dense Jacobi eigensolve of G; default 256 */
+  double tol;        /* convergence: every wanted Ritz pair has ||G x - theta x|| <= tol * theta_k (theta_k =
+                        the k-th Ritz value, not theta_1), or -- where theta_k / theta_{k+1} < 1.05 -- the
+                        Kato-Temple estimate of the remaining Ky Fan deficit is <= tol / 5 of the wanted
+                        energy not yet locked; default 1e-6 */
+  int dense_max_m;   /* m <= this (<= 256): one dense eigensolve of G; default 256 */
   int gemm_chain;    /* tuning: K-chunks per TMEM accumulation chain (0 = default) */
   int gemm_splits;   /* tuning: K splits of the Gram (0 = auto) */
   const float* init_S; /* optional DEVICE [k][m] warm start of the subspace iteration (e.g. the sketch of
@@ -99,18 +116,16 @@ typedef struct {
                           and return TSK_ENONFINITE if any entry is NaN or Inf (matrices are
                           finite); device inputs: nothing is computed; host inputs are checked per staged
                           chunk, so G64 is unspecified after the error */
-  int cheb_degree;     /* cap on the Chebyshev filter degree per outer iteration (0 = adaptive, <= 12: the
-                          largest degree whose dynamic range T_d(x_max) stays <= 1e6) */
-  int tol_active;      /* != 0: once dominant pairs are locked, Ritz residuals are measured against the top
-                          of the remaining (deflated) spectrum instead of theta_1 -- tighter eigenvectors
-                          below a dominant eigenvalue (e.g. a frame mean), more iterations; max_resid is
-                          then reported on that scale */
+  int cheb_degree;     /* cap on the Chebyshev filter degree per outer iteration (0 = adaptive, <= 40: the
+                          largest degree whose dynamic range T_d(x_max) stays <= 1e7) */
+  int tol_active;      /* kept for ABI compatibility, ignored: residuals are always measured against theta_k
+                          (the semantics this flag used to select) */
 } tsk_train_opts;
 
 typedef struct {
   int iters;          /* subspace iterations run (0 for the dense path) */
   double kyfan;       /* sum_{i<k} theta_i, the Ky Fan energy tr(S G S^T) */
-  double max_resid;   /* max_{i<k} ||G s_i - theta_i s_i|| / theta_1 (/ the active top with tol_active) */
+  double max_resid;   /* max_{i<k} ||G s_i - theta_i s_i|| / theta_k over the pairs not yet locked */
   int gram_splits;    /* K splits used by the Gram kernel */
   int gram_tiles;     /* 128x128 output tiles computed (lower triangle) */
   double gap_est;     /* theta_k / theta_{k+1} from the last Rayleigh-Ritz step (the eigengap of reading c6;

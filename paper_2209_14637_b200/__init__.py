@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 import warnings
 from typing import Optional
 
@@ -34,7 +35,7 @@ EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_stat
             "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2",
             "sketch_train_two_sided", "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe",
             "tsk_eig_probe", "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init",
-            "tsk_syev_probe"]
+            "tsk_syev_probe", "tsk_allgather_errors", "tsk_allreduce_gram"]
 
 
 class TskError(RuntimeError):
@@ -117,12 +118,14 @@ def lib() -> ctypes.CDLL:
         L.tsk_gram_probe.argtypes = [vp, f32p, i64, i32, i32, f64p, i32, i32, i32]
         L.tsk_eig_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp]
         L.tsk_syev_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp, ctypes.c_double]
+        L.tsk_allgather_errors.argtypes = [vp, f64p, i64, f64p]
+        L.tsk_allreduce_gram.argtypes = [vp, f64p, i32]
         L.sketch_train_matrix_free.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, vp, vp]
         L.tsk_get_unique_id.argtypes = [vp]
         L.tsk_comm_init.argtypes = [vp, i32, i32, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
                   "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2", "sketch_train_two_sided",
-                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe", "tsk_syev_probe",
+                  "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe", "tsk_syev_probe", "tsk_allgather_errors", "tsk_allreduce_gram",
                   "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"):
             getattr(L, f).restype = i32
         _lib = L
@@ -201,17 +204,42 @@ def get_unique_id() -> bytes:
 
 
 _ctx_cache: dict = {}
+_ctx_lock = threading.Lock()
 
 
 def context(device=None) -> Context:
+    """The default context of (device, current torch stream, calling thread): a ctx owns workspaces that
+    its queued work uses, so two threads or two streams never share one (include/tsketch.h: one ctx per
+    thread / stream)."""
     if device is None:
         device = torch.cuda.current_device()
-    key = torch.device("cuda", device).index if isinstance(device, int) else torch.device(device).index
-    if key not in _ctx_cache:
-        _ctx_cache[key] = Context(key)
-    ctx = _ctx_cache[key]
+    dev = torch.device("cuda", device).index if isinstance(device, int) else torch.device(device).index
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    key = (dev, stream, threading.get_ident())
+    with _ctx_lock:
+        ctx = _ctx_cache.get(key)
+        if ctx is None:
+            ctx = _ctx_cache[key] = Context(dev)
     ctx._bind_stream()
     return ctx
+
+
+def allreduce_gram(G64: torch.Tensor, ctx: Optional[Context] = None) -> torch.Tensor:
+    """tsk_allreduce_gram: sum G64 [m, m] (cuda fp64) in place over the library's NCCL communicator."""
+    _need(G64, torch.float64, "G64", 2)
+    ctx = ctx or context(G64.device)
+    _check(lib().tsk_allreduce_gram(ctx.handle, _ptr(G64), G64.shape[0]), "tsk_allreduce_gram")
+    return G64
+
+
+def allgather_errors(err_local: torch.Tensor, B_total: int, ctx: Optional[Context] = None) -> torch.Tensor:
+    """tsk_allgather_errors: the per-matrix errors of all ranks' contiguous test shards, in stream order,
+    on every rank (the library's NCCL communicator from tsk_comm_init; a copy without one)."""
+    _need(err_local, torch.float64, "err_local", 1)
+    ctx = ctx or context(err_local.device)
+    out = torch.empty((int(B_total),), dtype=torch.float64, device=err_local.device)
+    _check(lib().tsk_allgather_errors(ctx.handle, _ptr(err_local), int(B_total), _ptr(out)), "tsk_allgather_errors")
+    return out
 
 
 def _ptr(t: Optional[torch.Tensor]):

@@ -34,6 +34,9 @@ tsk_status cuda_ok(cudaError_t e) {
 
 bool is_error(tsk_status s) { return (int)s < 0; }
 
+// device fp32 matrices are read with float4 / TMA: 16-byte alignment (host inputs are staged)
+bool misaligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
 // Device view of a possibly-host buffer: allocated from a dedicated ctx workspace slot.
 struct DevBuf {
   void* dev = nullptr;
@@ -60,6 +63,7 @@ struct CtxExt {
   size_t buf_bytes = 0;
   void* dev_small[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t dev_small_bytes[4] = {0, 0, 0, 0};
+  cudaEvent_t handoff = nullptr;  // tsk_set_stream: the new stream waits for the old one
 };
 
 struct tsk_ctx_full {
@@ -112,6 +116,7 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 static NcclApi* nccl_api() {
@@ -126,7 +131,8 @@ static NcclApi* nccl_api() {
     api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
     api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
     api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
-    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy;
+    api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(h, "ncclAllGather"));
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.allGather;
   });
   return api.ok ? &api : nullptr;
 }
@@ -141,7 +147,37 @@ tsk_status allreduce_gram(Ctx* c, double* G, size_t n) {
     return TSK_ENCCL;
   return TSK_OK;
 }
+// every rank learns the worst status of the pre-collective phase (ncclMin over int32: errors are
+// negative), so a rank that fails before the Gram all-reduce cannot leave its peers blocked in it
+tsk_status allreduce_status(Ctx* c, tsk_status local) {
+  if (!c->comm) return local;
+  NcclApi* api = nccl_api();
+  if (!api) return TSK_ENCCL;
+  int* d = reinterpret_cast<int*>(c->workspace(WS_CHECK, 64));
+  int* h = reinterpret_cast<int*>(c->pinned(64));
+  if (!d || !h) return TSK_ENOMEM;
+  h[0] = (int)local;
+  if (cudaMemcpyAsync(d, h, sizeof(int), cudaMemcpyHostToDevice, c->stream) != cudaSuccess) return TSK_ECUDA;
+  if (api->allReduce(d, d, 1, ncclInt32, ncclMin, reinterpret_cast<ncclComm_t>(c->comm), c->stream) != ncclSuccess)
+    return TSK_ENCCL;
+  if (cudaMemcpyAsync(h, d, sizeof(int), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return TSK_ECUDA;
+  return (tsk_status)std::min(h[0], (int)local);
+}
 }  // namespace tsk
+
+// out[b] = pad[rank(b)][b - lo(rank(b))]: compaction of the padded all-gather of contiguous shards
+__global__ void unpad_gather_kernel(const double* __restrict__ pad, long long per, long long B, int P,
+                                    double* __restrict__ out) {
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  // rank of index b under shard_range: the largest p with floor(p B / P) <= b
+  long long p = (b * P) / B;
+  while (p + 1 < P && ((p + 1) * B) / P <= b) ++p;
+  while (p > 0 && (p * B) / P > b) --p;
+  out[b] = pad[p * per + (b - (p * B) / P)];
+}
 
 extern "C" {
 
@@ -176,6 +212,46 @@ tsk_status tsk_comm_init(tsk_ctx ctx, int nranks, int rank, const unsigned char 
   c.nranks = nranks;
   c.rank = rank;
   return TSK_OK;
+}
+
+tsk_status tsk_allreduce_gram(tsk_ctx ctx, double* G64, int m) {
+  if (!ctx) return TSK_ENULL;
+  if (!G64) return TSK_ENULL;
+  if (m < 1) return TSK_EINVAL;
+  if (!is_device_ptr(G64)) return TSK_EINVAL;
+  cudaSetDevice(ctx->c.device);
+  return tsk::allreduce_gram(&ctx->c, G64, (size_t)m * m);
+}
+
+tsk_status tsk_allgather_errors(tsk_ctx ctx, const double* err_local, int64_t B_total, double* err_all) {
+  if (!ctx) return TSK_ENULL;
+  if (B_total < 0) return TSK_EINVAL;
+  Ctx& c = ctx->c;
+  const int P = c.comm ? c.nranks : 1, rank = c.comm ? c.rank : 0;
+  const int64_t lo = (int64_t)rank * B_total / P, hi = (int64_t)(rank + 1) * B_total / P;
+  if (B_total == 0) return TSK_OK;
+  if (!err_all || (hi > lo && !err_local)) return TSK_ENULL;
+  if (!is_device_ptr(err_all) || (hi > lo && !is_device_ptr(err_local))) return TSK_EINVAL;
+  cudaSetDevice(c.device);
+  if (!c.comm)
+    return cuda_ok(cudaMemcpyAsync(err_all, err_local, (size_t)B_total * 8, cudaMemcpyDeviceToDevice, c.stream));
+  NcclApi* api = nccl_api();
+  if (!api) return TSK_ENCCL;
+  // shards differ by at most one: pad to the largest, gather [P][per], compact in shard order
+  const int64_t per = (B_total + P - 1) / P;
+  double* pad = reinterpret_cast<double*>(c.workspace(tsk::WS_GATHER, (size_t)(P + 1) * per * 8));
+  if (!pad) return TSK_ENOMEM;
+  double* mine = pad + (size_t)P * per;
+  if (cudaMemsetAsync(mine, 0, (size_t)per * 8, c.stream) != cudaSuccess) return TSK_ECUDA;
+  if (hi > lo && cudaMemcpyAsync(mine, err_local, (size_t)(hi - lo) * 8, cudaMemcpyDeviceToDevice, c.stream) !=
+                     cudaSuccess)
+    return TSK_ECUDA;
+  if (api->allGather(mine, pad, (size_t)per, ncclFloat64, reinterpret_cast<ncclComm_t>(c.comm), c.stream) !=
+      ncclSuccess)
+    return TSK_ENCCL;
+  unpad_gather_kernel<<<(unsigned)((B_total + 255) / 256), 256, 0, c.stream>>>(pad, per, B_total, P, err_all);
+  c.count_launch();
+  return tsk::launch_status("tsk_allgather_errors");
 }
 
 const char* tsk_status_string(tsk_status s) {
@@ -242,13 +318,23 @@ tsk_status tsk_destroy(tsk_ctx ctx) {
   for (int i = 0; i < 4; ++i)
     if (e->dev_small[i]) cudaFree(e->dev_small[i]);
   if (e->copy) cudaStreamDestroy(e->copy);
+  if (e->handoff) cudaEventDestroy(e->handoff);
   delete reinterpret_cast<tsk_ctx_full*>(ctx);
   return TSK_OK;
 }
 
 tsk_status tsk_set_stream(tsk_ctx ctx, void* cuda_stream) {
   if (!ctx) return TSK_ENULL;
-  ctx->c.stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  Ctx& c = ctx->c;
+  cudaStream_t ns = reinterpret_cast<cudaStream_t>(cuda_stream);
+  if (ns == c.stream) return TSK_OK;
+  // work still queued on the old stream uses this ctx's workspaces: the new stream waits for it
+  cudaSetDevice(c.device);
+  CtxExt* e = ext_of(ctx);
+  if (!e->handoff && cudaEventCreateWithFlags(&e->handoff, cudaEventDisableTiming) != cudaSuccess) return TSK_ECUDA;
+  if (cudaEventRecord(e->handoff, c.stream) != cudaSuccess || cudaStreamWaitEvent(ns, e->handoff, 0) != cudaSuccess)
+    return TSK_ECUDA;
+  c.stream = ns;
   return TSK_OK;
 }
 
@@ -370,7 +456,8 @@ static tsk_status gram_host(tsk_ctx ctx, const float* A, int64_t D, int m, int n
     if (is_error(s)) return s;
     cudaEventRecord(e->consumed[i], c->stream);
   }
-  return TSK_OK;
+  // host inputs are synchronous (include/tsketch.h): the caller may refill its buffer on return
+  return cuda_ok(cudaStreamSynchronize(c->stream));
 }
 
 tsk_status sketch_gram(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, float* G32, int accumulate,
@@ -379,6 +466,7 @@ tsk_status sketch_gram(tsk_ctx ctx, const float* A, int64_t D, int m, int n, dou
   if (!A || !G64) return TSK_ENULL;
   if (D < 1 || m < 1 || n < 1) return TSK_EINVAL;
   if (n % 4) return TSK_ESHAPE;
+  if (is_device_ptr(A) && misaligned16(A)) return TSK_ESHAPE;
   Ctx* c = &ctx->c;
   cudaSetDevice(c->device);
   DevBuf g64, g32;
@@ -403,12 +491,20 @@ tsk_status sketch_gram(tsk_ctx ctx, const float* A, int64_t D, int m, int n, dou
   return TSK_OK;
 }
 
+// the eigensolver's Rayleigh-Ritz block p = min(m, k + oversample) must be <= 128 above the dense path
+static bool block_ok(int m, int k, const tsk_train_opts* opts) {
+  const int dense = opts && opts->dense_max_m > 0 ? std::min(opts->dense_max_m, 256) : 256;
+  const int q = opts && opts->oversample > 0 ? opts->oversample : 16;
+  const int p = std::min(m, k + q);
+  return m <= dense || p >= m ? m <= 256 : p <= 128;
+}
+
 tsk_status sketch_topk(tsk_ctx ctx, const double* G64, int m, int k, float* S, double* lambda,
                        const tsk_train_opts* opts, tsk_train_info* info) {
   if (!ctx) return TSK_ENULL;
   if (!G64 || !S) return TSK_ENULL;
   if (m < 1 || k < 1 || k > m) return TSK_EINVAL;
-  if (m > 256 && k + 16 > 256) return TSK_EINVAL;  // Rayleigh-Ritz block p = k + 16 <= 256
+  if (!block_ok(m, k, opts)) return TSK_EINVAL;
   cudaSetDevice(ctx->c.device);
   DevBuf g, sb, lb;
   tsk_status s = stage_slot(ctx, G64, (size_t)m * m * 8, 0, g, true);
@@ -427,25 +523,34 @@ tsk_status sketch_topk(tsk_ctx ctx, const double* G64, int m, int k, float* S, d
 tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S, double* lambda,
                         double* G64_out, const tsk_train_opts* opts, tsk_train_info* info) {
   if (!ctx) return TSK_ENULL;
-  if (!A || !S) return TSK_ENULL;
-  if (D < 1 || m < 1 || n < 1 || k < 1 || k > m) return TSK_EINVAL;
-  if (m > 256 && k + 16 > 256) return TSK_EINVAL;  // Rayleigh-Ritz block p = k + 16 <= 256
-  if (n % 4) return TSK_ESHAPE;
   Ctx* c = &ctx->c;
   cudaSetDevice(c->device);
+  // Validation and the local Gram must not return early on a multi-rank communicator: every rank
+  // joins the status all-reduce (below) so a failing rank cannot leave its peers in the Gram
+  // all-reduce.  With a communicator a rank may own no training matrix (D = 0: zero contribution).
+  tsk_status pre = TSK_OK;
+  if (!S || (D > 0 && !A)) pre = TSK_ENULL;
+  else if (D < (c->comm ? 0 : 1) || m < 1 || n < 1 || k < 1 || k > m || !block_ok(m, k, opts)) pre = TSK_EINVAL;
+  else if (n % 4 || (D > 0 && is_device_ptr(A) && misaligned16(A))) pre = TSK_ESHAPE;
   double* G = nullptr;
   const bool g_dev = G64_out && is_device_ptr(G64_out);
-  if (g_dev) {
-    G = G64_out;
-  } else {
-    G = reinterpret_cast<double*>(c->workspace(tsk::WS_GRAM, (size_t)m * m * 8));
-    if (!G) return TSK_ENOMEM;
+  if (pre == TSK_OK) {
+    if (g_dev) {
+      G = G64_out;
+    } else {
+      G = reinterpret_cast<double*>(c->workspace(tsk::WS_GRAM, (size_t)m * m * 8));
+      if (!G) pre = TSK_ENOMEM;
+    }
   }
-  tsk_status s;
-  if (is_device_ptr(A))
-    s = gram_device(c, A, D, m, n, G, nullptr, 0, opts, info);
-  else
-    s = gram_host(ctx, A, D, m, n, G, nullptr, 0, opts, info);
+  if (pre == TSK_OK) {
+    if (D == 0)
+      pre = cuda_ok(cudaMemsetAsync(G, 0, (size_t)m * m * 8, c->stream));
+    else if (is_device_ptr(A))
+      pre = gram_device(c, A, D, m, n, G, nullptr, 0, opts, info);
+    else
+      pre = gram_host(ctx, A, D, m, n, G, nullptr, 0, opts, info);
+  }
+  tsk_status s = tsk::allreduce_status(c, pre);
   if (is_error(s)) return s;
   if (is_error(s = tsk::allreduce_gram(c, G, (size_t)m * m))) return s;  // multi-GPU (tsk_comm_init)
   DevBuf sb, lb;
@@ -471,6 +576,7 @@ static tsk_status scw_common(tsk_ctx ctx, const float* A, int64_t B, int m, int 
   if (B < 0 || m < 1 || n < 1 || k < 1 || k > m || r < 1) return TSK_EINVAL;
   if (B > 0 && (!A || !S)) return TSK_ENULL;
   if (n % 4) return TSK_ESHAPE;
+  if (B > 0 && is_device_ptr(A) && misaligned16(A)) return TSK_ESHAPE;
   if (k > 128) return TSK_EINVAL;
   tsk_status warn = TSK_OK;
   if (r > k) {
@@ -501,9 +607,11 @@ static tsk_status scw_common(tsk_ctx ctx, const float* A, int64_t B, int m, int 
     Ad = reinterpret_cast<float*>(c->workspace(tsk::WS_HOST_IN, (size_t)chunk * mat));
     if (!Ad) return TSK_ENOMEM;
   }
-  const size_t out_per = ((L ? (size_t)m * r * 4 : 0) + (R ? (size_t)n * r * 4 : 0) + (sigma ? (size_t)r * 4 : 0) +
-                          (err ? 8 : 0) + 64);
-  uint8_t* Od = reinterpret_cast<uint8_t*>(c->workspace(tsk::WS_HOST_OUT, (size_t)chunk * out_per + 256));
+  // staging for host outputs, sized with the same 256-byte rounding carve() applies per array
+  auto r256 = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t out_bytes = (L ? r256((size_t)chunk * m * r * 4) : 0) + (R ? r256((size_t)chunk * n * r * 4) : 0) +
+                           (sigma ? r256((size_t)chunk * r * 4) : 0) + (err ? r256((size_t)chunk * 8) : 0) + 256;
+  uint8_t* Od = reinterpret_cast<uint8_t*>(c->workspace(tsk::WS_HOST_OUT, out_bytes));
   if (!Od) return TSK_ENOMEM;
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t bc = std::min<int64_t>(chunk, B - b0);

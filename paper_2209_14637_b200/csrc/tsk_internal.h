@@ -68,6 +68,7 @@ enum WorkspaceId {
   WS_CHECK,        // input validation flag (check_finite)
   WS_EIG_GQ,       // eigensolver: split-K partial tiles + tickets of the fp64 product
   WS_SYEV,         // small symmetric eigensolver: reflectors, tridiagonal, scratch
+  WS_GATHER,       // tsk_allgather_errors: padded [P][per] gather buffer
   WS_COUNT
 };
 

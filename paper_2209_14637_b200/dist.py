@@ -29,6 +29,27 @@ def reduce_gram(G64: torch.Tensor, group=None) -> torch.Tensor:
     return G64
 
 
+def gather_errors(err_local: torch.Tensor, B_total: int, group=None) -> torch.Tensor:
+    """All ranks' per-matrix test errors in stream order on every rank (the torch.distributed route of
+    tsk_allgather_errors): rank p holds matrices shard_range(B_total, p, P); the shards are padded to
+    ceil(B/P), all-gathered, and compacted.  The paper's test error is a mean over
+    the whole test set, so it needs every rank's errors."""
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    if world == 1:
+        return err_local.clone()
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(B_total, rank, world)
+    if err_local.numel() != hi - lo:
+        raise ValueError(f"rank {rank} holds {err_local.numel()} errors, its shard has {hi - lo}")
+    per = -(-B_total // world)
+    pad = torch.zeros(per, dtype=err_local.dtype, device=err_local.device)
+    pad[: hi - lo] = err_local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([parts[p][: shard_range(B_total, p, world)[1] - shard_range(B_total, p, world)[0]]
+                      for p in range(world)])
+
+
 def init_native_comm(ctx=None, group=None):
     """Give the library its own NCCL communicator over the ranks of `group` (tsk_comm_init): rank 0
     draws the unique id, torch.distributed broadcasts it.  Afterwards ``sketch_train`` all-reduces the
@@ -45,13 +66,25 @@ def init_native_comm(ctx=None, group=None):
     return ctx
 
 
-def train(A_local: torch.Tensor, k: int, group=None, opts=None, G64: Optional[torch.Tensor] = None):
+def train(A_local: torch.Tensor, k: int, group=None, opts=None, G64: Optional[torch.Tensor] = None,
+          gram_fn=None, topk_fn=None):
     """Algorithm 2 lines 1-2 over all ranks of `group`: local Gram of this rank's shard,
-    all-reduce, top-k eigenvectors.  Returns (S [k, m], lambda [k], info, status)."""
+    all-reduce, top-k eigenvectors.  Returns (S [k, m], lambda [k], info, status).
+    gram_fn / topk_fn default to the library's sketch_gram / sketch_topk (the CPU multi-process tests
+    substitute fp64 stand-ins to exercise this control flow without a GPU)."""
     from . import sketch_gram, sketch_topk
 
-    G64, ginfo = sketch_gram(A_local, G64=G64, opts=opts)
+    sketch_gram = gram_fn or sketch_gram
+    sketch_topk = topk_fn or sketch_topk
+
+    if A_local.shape[0] == 0:  # an empty shard still joins the all-reduce (zero contribution)
+        m = A_local.shape[1]
+        G64 = torch.zeros((m, m), dtype=torch.float64, device=A_local.device) if G64 is None else G64.zero_()
+        ginfo = None
+    else:
+        G64, ginfo = sketch_gram(A_local, G64=G64, opts=opts)
     reduce_gram(G64, group)
     S, lam, info, st = sketch_topk(G64, k, opts=opts)
-    info.gram_splits, info.gram_tiles = ginfo.gram_splits, ginfo.gram_tiles
+    if ginfo is not None:
+        info.gram_splits, info.gram_tiles = ginfo.gram_splits, ginfo.gram_tiles
     return S, lam, info, st

@@ -339,9 +339,43 @@ def test_native_nccl_communicator_single_rank():
     S1, lam1, _, _ = tsk.sketch_train(A, c.k, ctx=ctx)
     torch.cuda.synchronize()
     assert torch.equal(S0, S1) and torch.equal(lam0, lam1)
+    # the split route of bench.py: sketch_gram -> tsk_allreduce_gram -> sketch_topk, same sketch
+    G = torch.empty(c.m, c.m, dtype=torch.float64, device="cuda")
+    tsk.sketch_gram(A, G64=G, ctx=ctx)
+    G0 = G.clone()
+    tsk.allreduce_gram(G, ctx=ctx)
+    S2, lam2, _, _ = tsk.sketch_topk(G, c.k, ctx=ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(G, G0) and torch.equal(S2, S0)
+    # errors of the (single) shard gathered in stream order; an empty local shard with B_total = 0
+    T = datagen.generate(c, "test", 0, 7).cuda()
+    e = tsk.scw_error(T, S1, c.r, ctx=ctx)
+    assert torch.equal(tsk.allgather_errors(e, 7, ctx=ctx), e)
+    assert tsk.allgather_errors(e[:0], 0, ctx=ctx).numel() == 0
+    # with a communicator a rank may own no training matrix (zero contribution, still joins the collectives)
+    Sz, lamz, _, stz = tsk.sketch_train(A[:0], c.k, ctx=ctx)
+    torch.cuda.synchronize()
+    assert torch.allclose(Sz.double() @ Sz.double().T, torch.eye(c.k, dtype=torch.float64, device="cuda"), atol=1e-5)
     with pytest.raises(tsk.TskError):
         ctx.comm_init(2, 2, uid)  # rank outside [0, nranks)
     ctx.close()
+    # without a communicator an empty stack is an argument error
+    with pytest.raises(tsk.TskError):
+        tsk.sketch_train(A[:0], c.k)
+
+
+def test_misaligned_device_input_is_a_shape_error():
+    """a device fp32 stack not 16-byte aligned is rejected up front (TSK_ESHAPE) instead of
+    faulting in the float4 / TMA reads."""
+    A = torch.zeros(2 * 64 * 48 + 1, device="cuda")
+    Am = A[1:].view(2, 64, 48)
+    with pytest.raises(tsk.TskError) as e:
+        tsk.sketch_gram(Am)
+    assert e.value.status == -2
+    S = torch.eye(10, 64, device="cuda")
+    with pytest.raises(tsk.TskError) as e:
+        tsk.scw_error(Am, S, 5)
+    assert e.value.status == -2
 
 
 def test_check_finite_rejects_nan_and_inf():
@@ -380,3 +414,32 @@ def test_tol_active_tightens_the_non_dominant_subspace():
     assert st0 == 0 and st1 == 0
     d0, d1 = non_dominant_deficit(S0), non_dominant_deficit(S1)
     assert d1 <= 1e-6 and d1 <= d0, (d0, d1)
+
+
+def test_host_outputs_small_batch_staging():
+    """host L / R / sigma for B = 1, m = 65, n = 68, r = 1 (the 256-byte carve rounding used to
+    place sigma past the end of the staging buffer): identical to the device-output path."""
+    g = torch.Generator().manual_seed(5)
+    T = torch.rand(1, 65, 68, generator=g)
+    S = torch.tensor(np.linalg.qr(np.random.default_rng(1).standard_normal((65, 3)))[0].T.copy(),
+                     dtype=torch.float32)
+    L_d, R_d, s_d = tsk.sketch_apply_scw(T.cuda(), S.cuda(), 1)
+    L_h, R_h, s_h = tsk.sketch_apply_scw(T, S, 1)
+    assert torch.equal(L_h, L_d.cpu()) and torch.equal(R_h, R_d.cpu()) and torch.equal(s_h, s_d.cpu())
+
+
+def test_pinned_host_input_is_synchronous():
+    """a pinned host training stack may be refilled as soon as sketch_gram returns (streaming
+    use, accumulate): the H2D copies of the call have completed by then."""
+    c = datagen.CONFIGS["C2"]
+    A = datagen.generate(c, "train", 0, 40)
+    buf = torch.empty(20, c.m, c.n).pin_memory()
+    G = torch.empty(c.m, c.m, dtype=torch.float64, device="cuda")
+    buf.copy_(A[:20])
+    tsk.sketch_gram(buf, G64=G)
+    buf.copy_(A[20:])  # immediately overwrite the pinned buffer
+    tsk.sketch_gram(buf, G64=G, accumulate=True)
+    G_ref, _ = tsk.sketch_gram(A[:20].cuda())  # the same two chunks from device memory: bit-identical
+    tsk.sketch_gram(A[20:].cuda(), G64=G_ref, accumulate=True)
+    torch.cuda.synchronize()
+    assert torch.equal(G, G_ref)
