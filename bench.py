@@ -368,7 +368,16 @@ def run_tsketch(args, c):
             dist.destroy_process_group()
         return
     mp, peak_kind = measured_peaks()
-    peak_tf32 = mp["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
+    derived_tf32 = mp["bf16_tflops_sustained"] * NOMINAL_TF32_OVER_BF16
+    # the measured dense TF32 peak of this pool's B200 (scripts/tf32_peak.py: cuBLAS TF32 8192^3, burst and
+    # 4 s sustained); the Gram runs ~22 ms per launch at the burst clocks (bench clocks median ~1.9 GHz),
+    # so the burst figure is the denominator (the sustained one is taken at power-capped clocks)
+    tf32 = None
+    try:
+        tf32 = json.load(open(os.path.join(ROOT, "profiles", "r02_tf32_peak.json")))
+    except Exception:
+        tf32 = None
+    peak_tf32 = tf32["tf32_tflops_cublas_burst"] if tf32 else derived_tf32
     dloc = d1 - d0
     alg_flops = c.m * (c.m + 1) * c.n * dloc     # lower-triangle Gram, per launch (this rank's shard)
     gram_ms = phases["gram"]
@@ -397,8 +406,13 @@ def run_tsketch(args, c):
                 "frac": achieved / peak_tf32, "traffic": traffic,
                 "kernel": "gram_pair_kernel (tcgen05 cta_group::2, 3xTF32 lower-triangle Gram) + finalize",
                 "algorithmic_flops_per_launch": alg_flops,
-                "peak_note": f"TF32 = {peak_kind} bf16 sustained {mp['bf16_tflops_sustained']} TF/s x nominal "
-                             f"1.1/2.25 (B200_PROFILING.md)",
+                "peak_note": (f"TF32 measured on this pool's B200 (profiles/r02_tf32_peak.json, cuBLAS TF32 8192^3): "
+                              f"burst {tf32['tf32_tflops_cublas_burst']:.1f}, sustained "
+                              f"{tf32['tf32_tflops_cublas_sustained']:.1f} TF/s; burst used (the Gram runs at burst "
+                              f"clocks); {peak_kind} bf16 sustained x 1.1/2.25 would give {derived_tf32:.1f}"
+                              if tf32 else f"TF32 = {peak_kind} bf16 sustained {mp['bf16_tflops_sustained']} TF/s x "
+                              f"nominal 1.1/2.25 (B200_PROFILING.md)"),
+                "issued_frac_of_measured_tf32": issued_area / (gram_ms / 1e3) / 1e12 / peak_tf32,
                 "issued_tflops": issued_area / (gram_ms / 1e3) / 1e12,
                 "issued_frac_of_nominal_tf32": issued_area / (gram_ms / 1e3) / 1.1e15,
                 "gram_ms_per_launch": gram_ms}
