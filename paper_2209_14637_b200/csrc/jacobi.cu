@@ -44,7 +44,9 @@ __device__ __forceinline__ void rr_pair(int r, int k, int pe, int& i, int& j) {
 template <bool kSmem, int NQ, int KQ>
 __global__ void __launch_bounds__(kJacThreads)
     jacobi_eig_kernel(const double* __restrict__ H, int p, double* __restrict__ W, double* __restrict__ lam,
-                      double* __restrict__ gscratch, int max_sweeps, double tol, int* __restrict__ sweeps_out) {
+                      double* __restrict__ gscratch, int max_sweeps, double tol, int* __restrict__ sweeps_out,
+                      const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;  // uniform: device-side fallback not needed
   extern __shared__ double jsm[];
   __shared__ int rot_count;
   __shared__ double lam_s[256];
@@ -182,17 +184,17 @@ __global__ void __launch_bounds__(kJacThreads)
 
 template <bool kSmem, int NQ, int KQ>
 static void launch_jacobi(int batch, int threads, size_t smem, cudaStream_t st, const double* H, int p, double* W,
-                          double* lam, double* scratch, double tol, int* sweeps) {
+                          double* lam, double* scratch, double tol, int* sweeps, const int* gate) {
   static uint64_t attr = 0;
   if (kSmem && !(attr & device_bit())) {
     cudaFuncSetAttribute(jacobi_eig_kernel<kSmem, NQ, KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kJacSmemMax);
     attr |= device_bit();
   }
-  jacobi_eig_kernel<kSmem, NQ, KQ><<<batch, threads, smem, st>>>(H, p, W, lam, scratch, 30, tol, sweeps);
+  jacobi_eig_kernel<kSmem, NQ, KQ><<<batch, threads, smem, st>>>(H, p, W, lam, scratch, 30, tol, sweeps, gate);
 }
 
 tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps,
-                              double tol) {
+                              double tol, const int* gate) {
   if (p < 1 || p > 256 || batch < 0) return TSK_EINVAL;
   if (batch == 0) return TSK_OK;
   const size_t need = (size_t)2 * p * (p + 1) * sizeof(double);
@@ -209,12 +211,12 @@ tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, doubl
   const int threads = std::min(kJacThreads, std::max(64, ((p + 1) / 2 * 16 + 31) / 32 * 32));
   cudaStream_t st = ctx->stream;
   if (use_smem) {
-    if (p <= 32) launch_jacobi<true, 2, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps);
-    else if (p <= 64) launch_jacobi<true, 4, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps);
-    else launch_jacobi<true, 8, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps);
+    if (p <= 32) launch_jacobi<true, 2, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps, gate);
+    else if (p <= 64) launch_jacobi<true, 4, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps, gate);
+    else launch_jacobi<true, 8, 1>(batch, threads, smem, st, H, p, W, lam, nullptr, tol, sweeps, gate);
   } else {
-    if (p <= 128) launch_jacobi<false, 8, 1>(batch, threads, 0, st, H, p, W, lam, scratch, tol, sweeps);
-    else launch_jacobi<false, 16, 2>(batch, threads, 0, st, H, p, W, lam, scratch, tol, sweeps);
+    if (p <= 128) launch_jacobi<false, 8, 1>(batch, threads, 0, st, H, p, W, lam, scratch, tol, sweeps, gate);
+    else launch_jacobi<false, 16, 2>(batch, threads, 0, st, H, p, W, lam, scratch, tol, sweeps, gate);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return TSK_ECUDA;
   ctx->count_launch();

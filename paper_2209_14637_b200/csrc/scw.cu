@@ -107,12 +107,17 @@ __global__ void scw_sigma_kernel(const double* __restrict__ sig2, int k, int r, 
   sigma[idx] = (float)sqrt(fmax(sig2[b * k + c], 0.0));
 }
 
+// err[b] = sqrt(sum of the b-th matrix's residual partials): one warp per matrix, lanes strided, fixed-
+// order butterfly (deterministic)
 __global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles, long long B, double* __restrict__ err) {
-  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (b >= B) return;
   double s = 0.0;
-  for (int t = 0; t < tiles; ++t) s += part[b * tiles + t];
-  err[b] = sqrt(s);
+  for (int t = lane; t < tiles; t += 32) s += part[b * tiles + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) err[b] = sqrt(s);
 }
 
 // ---------------------------------------------------------------- C = X X^T, register-tiled fp64
@@ -362,7 +367,7 @@ static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, c
   tsk_status st = gemm_tf32x3(ctx, gp);
   if (st != TSK_OK) return st;
   const int per = (int)(nb(m, 128) * nb(n, 128)) * 8;  // partials per matrix
-  scw_err_reduce_kernel<<<nb(bc, 128), 128, 0, ctx->stream>>>(part, per, bc, err);
+  scw_err_reduce_kernel<<<nb((long long)bc * 32, 256), 256, 0, ctx->stream>>>(part, per, bc, err);
   ctx->count_launch();
   return launch_status("scw residual (tcgen05)");
 }
@@ -389,7 +394,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   float* Bm_all = reinterpret_cast<float*>(ctx->workspace(WS_SCW_0, chunk * kn * 4));
   float* Vt_all = reinterpret_cast<float*>(ctx->workspace(WS_SCW_1, chunk * kn * 4));
   float* Zt_all = reinterpret_cast<float*>(ctx->workspace(WS_SCW_2, chunk * km * 4));
-  double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW_3, chunk * (4 * kk + 2 * k) * 8));
+  // small matrices per matrix + one int flag per possible part offset (the eigensolver fallback gate)
+  double* small = reinterpret_cast<double*>(ctx->workspace(WS_SCW_3, chunk * (4 * kk + 2 * k) * 8 + chunk * 4 + 64));
   const int tiles = (int)(nb(n, 128) * nb(m, 128)) * 8;  // residual partials per matrix
   // factor row pitch: r for the caller's L / R, r rounded up to 4 (16-byte TMA rows) for the error path
   const int ldf = (L || R) ? r : (r + 3) & ~3;
@@ -499,7 +505,16 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     launch_gram_rows_tiled(Zt, k, m, bc, H, s);
     ctx->count_launch(1);
     if ((st = launch_status("scw gram(AV)")) != TSK_OK) return st;
-    if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10)) != TSK_OK) return st;
+    // top-r eigenpairs of (AV)^T (AV): the tridiagonal eigensolver (syev.cu) for the batch; a problem whose
+    // wanted eigenvalues form an unresolved cluster (e.g. rank(A) < r: a null cluster among them) sets the
+    // flag, and the Jacobi eigensolver -- enqueued behind it, gated on the flag on the device -- redoes the
+    // batch (no host round trip)
+    {
+      int* gflag = reinterpret_cast<int*>(small + chunk * (4 * kk + 2 * k)) + off;
+      cudaMemsetAsync(gflag, 0, sizeof(int), s);
+      if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k)) != TSK_OK) return st;
+      if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag)) != TSK_OK) return st;
+    }
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw + (size_t)off * m * ldf;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf + (size_t)off * n * ldf;

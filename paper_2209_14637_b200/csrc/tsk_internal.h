@@ -224,12 +224,17 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
 // lam [nw] decreasing; flag (device, may be null) set to 1 if the vectors are not orthonormal to orth_tol
 tsk_status syev_top(Ctx* ctx, const double* H, int p, int nw, double* W, int ldw, double* lam, int* flag,
                     double orth_tol);
+// the same for a batch: H [batch][p][p], W [batch][p][ldw], lam [batch][nw]; flag set if any problem fails
+tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch, double* W, int ldw, double* lam,
+                            int* flag, double orth_tol, long long lstride = 0);
 
 // batched symmetric PSD eigensolver (one-sided Jacobi), jacobi.cu
 // H: [batch][p][p] fp64 symmetric (row-major, read only).  W: [batch][p][p] fp64 eigenvectors as
 // COLUMNS (W[b][i][c] = component i of eigenvector c), lam: [batch][p] fp64 decreasing.
+// gate (device int, may be null): the kernel returns at once unless *gate != 0 (a device-side fallback
+// behind syev_top_batched's orthogonality flag, no host round trip)
 tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam,
-                              int* sweeps = nullptr, double tol = 1e-13);
+                              int* sweeps = nullptr, double tol = 1e-13, const int* gate = nullptr);
 
 }  // namespace tsk
 
