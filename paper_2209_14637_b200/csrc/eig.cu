@@ -874,6 +874,9 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     attr |= device_bit();
   }
 
+  // the block Gram + Cholesky overlap the product on a side stream (ctx side streams, created once)
+  const bool overlap = ctx->side_ready() && !getenv("TSK_EIG_SERIAL");
+  cudaStream_t side = overlap ? ctx->side[0] : nullptr;
   bool converged = false;
   int outer = 0;
   double max_res = 0.0, a_lo = 0.0;
@@ -890,7 +893,6 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     //      (Y and Z stay intact for the fallbacks)
     double* Q = X;
     double* GQ = GX;
-    if ((st = product(Y, nullptr, pa, 1.0, 0.0, 0.0, Z)) != TSK_OK) return st;
     // one CholQR pass (Yin, Zin) -> (Yout, Zout), flag[0] on breakdown
     auto cholqr_step = [&](const double* Yin, const double* Zin, double* Yout, double* Zout,
                            double shift) -> tsk_status {
@@ -910,8 +912,10 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       if (jacobi) r = jacobi_eig_batched(ctx, H, pa, 1, W, theta);
       else r = syev_top(ctx, H, pa, pa, W, pa, theta, flags + 1, 1e-8);
       if (r != TSK_OK) return r;
-      if ((r = gemm_nn_f64(ctx, Q, pa, 0, W, pa, 0, m, pa, pa, 1, nullptr, F0, pa, 0)) != TSK_OK) return r;
-      if ((r = gemm_nn_f64(ctx, GQ, pa, 0, W, pa, 0, m, pa, pa, 1, nullptr, F1, pa, 0)) != TSK_OK) return r;
+      // Ritz vectors Q W -> F0 and G'Q W -> F1 in one launch (a batch of two, W shared)
+      if ((r = gemm_nn_f64(ctx, Q, pa, (long long)(GQ - Q), W, pa, 0, m, pa, pa, 2, nullptr, F0, pa,
+                           (long long)(F1 - F0))) != TSK_OK)
+        return r;
       ritz_res_kernel<<<kr, 256, 0, s>>>(F1, F0, pa, theta, m, res);
       ctx->count_launch();
       if ((r = launch_status("eig rr")) != TSK_OK) return r;
@@ -921,7 +925,32 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       return cudaStreamSynchronize(s) == cudaSuccess ? TSK_OK : TSK_ECUDA;
     };
     cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
-    if ((st = cholqr_step(Y, Z, Q, GQ, 0.0)) != TSK_OK) return st;
+    if (!overlap) {
+      if ((st = product(Y, nullptr, pa, 1.0, 0.0, 0.0, Z)) != TSK_OK) return st;
+      if ((st = cholqr_step(Y, Z, Q, GQ, 0.0)) != TSK_OK) return st;
+    } else {
+      // the block's Gram and its Cholesky (one-CTA latency chain) on a side stream, concurrently with
+      // the product Z = G'Y on the main stream; joined before the triangular solve that needs both
+      cudaEventRecord(ctx->ev[0], s);
+      cudaStreamWaitEvent(side, ctx->ev[0], 0);
+      ctx->stream = side;
+      st = gemm_tn_f64(ctx, Y, pa, 0, Y, pa, 0, m, pa, pa, 1, M, pa, 0, 1, WS_EIG_SMALL);
+      if (st == TSK_OK) {
+        chol_scale_kernel<<<1, kCiThreads, (size_t)pa * (pa | 1) * 8, side>>>(M, pa, 1e-14, 0.0, Rs, Cn, Cn + p,
+                                                                              flags);
+        ctx->count_launch();
+      }
+      cudaEventRecord(ctx->ev[1], side);
+      ctx->stream = s;
+      if (st != TSK_OK) return st;
+      if ((st = product(Y, nullptr, pa, 1.0, 0.0, 0.0, Z)) != TSK_OK) return st;
+      cudaStreamWaitEvent(s, ctx->ev[1], 0);
+      trsm2_kernel<<<nblk(2LL * m, kTrsmRows), kTrsmRows,
+                     ((size_t)pa * pa + (size_t)kTrsmRows * (pa | 1) + 2 * (size_t)pa) * 8, s>>>(Y, Z, Cn + p, Rs, Cn,
+                                                                                             m, pa, Q, GQ);
+      ctx->count_launch();
+      if ((st = launch_status("eig cholqr")) != TSK_OK) return st;
+    }
     if ((st = rr_finish(false)) != TSK_OK) return st;
     const int* hfl = reinterpret_cast<const int*>(hostbuf + 2 * p);
     if (hfl[0]) {

@@ -95,6 +95,92 @@ __global__ void __launch_bounds__(128) scw_combine_kernel(const float* __restric
   }
 }
 
+// Tiled version (round 2): the CTA computes CT outputs c x 64 columns j of one matrix with the inputs
+// staged through shared memory 16 rows a at a time (fp32 -> fp64 on the way in); thread (cg, jg) owns
+// c = c0 + cg + (CT/4) u and j = j0 + jg + 16 v (u, v < 4): conflict-free / broadcast shared reads,
+// coalesced global loads and (kVt) stores.  The one-column-pair-per-thread kernel above re-read its
+// inputs from global memory once per 16 outputs (latency-bound, ~25 % of the fp64 rate).
+template <int CT, bool kVt>
+__global__ void __launch_bounds__(CT * 4) scw_combine2_kernel(const float* __restrict__ In,
+                                                              const double* __restrict__ W,
+                                                              const double* __restrict__ mu, int k, int len,
+                                                              int nout, int ldw, long long wst,
+                                                              float* __restrict__ Out, int ldo) {
+  constexpr int JT = 64, KC = 16, CG = CT / 4;
+  __shared__ double Ws[KC][CT + 1];
+  __shared__ double Is[KC][JT + 1];
+  __shared__ double sc[CT];
+  const int b = blockIdx.z, j0 = blockIdx.x * JT, c0 = blockIdx.y * CT;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int cg = tid >> 4, jg = tid & 15;
+  const double* Wb = W + (size_t)b * wst;
+  const float* Ib = In + (size_t)b * k * len;
+  for (int c = tid; c < CT; c += nt) {
+    double v = 1.0;
+    if (kVt && c0 + c < nout) {
+      const double m0 = mu[(size_t)b * k];
+      const double mc = mu[(size_t)b * k + c0 + c];
+      v = (mc > 0.0 && mc > 1e-13 * m0) ? 1.0 / sqrt(mc) : 0.0;
+    }
+    sc[c] = v;
+  }
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  for (int a0 = 0; a0 < k; a0 += KC) {
+    for (int e = tid; e < KC * CT; e += nt) {
+      const int kk = e / CT, cc = e % CT;
+      Ws[kk][cc] = (a0 + kk < k && c0 + cc < nout) ? Wb[(size_t)(a0 + kk) * ldw + c0 + cc] : 0.0;
+    }
+    for (int e = tid; e < KC * JT; e += nt) {
+      const int kk = e / JT, jj = e % JT;
+      Is[kk][jj] = (a0 + kk < k && j0 + jj < len) ? (double)Ib[(size_t)(a0 + kk) * len + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      double w[4], x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = Ws[kk][cg + CG * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) x[v] = Is[kk][jg + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(w[u], x[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+  float* Ob = Out + (size_t)b * (kVt ? (size_t)nout * len : (size_t)len * ldo);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + cg + CG * u;
+    if (c >= nout) continue;
+    const double scl = sc[cg + CG * u];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j = j0 + jg + 16 * v;
+      if (j >= len) continue;
+      if (kVt) Ob[(size_t)c * len + j] = (float)(acc[u][v] * scl);
+      else Ob[(size_t)j * ldo + c] = (float)(acc[u][v] * scl);
+    }
+  }
+}
+
+// Out = combination of the k rows of In by W (see scw_combine_kernel), tiled over (64 columns, CT outputs)
+template <bool kVt>
+static void launch_combine2(const float* In, const double* W, const double* mu, int k, int len, int nout, int ldw,
+                            long long wst, float* Out, int ldo, int batch, cudaStream_t s) {
+  if (nout <= 32)
+    scw_combine2_kernel<32, kVt><<<dim3((len + 63) / 64, 1, batch), 128, 0, s>>>(In, W, mu, k, len, nout, ldw, wst,
+                                                                                 Out, ldo);
+  else
+    scw_combine2_kernel<64, kVt><<<dim3((len + 63) / 64, (nout + 63) / 64, batch), 256, 0, s>>>(
+        In, W, mu, k, len, nout, ldw, wst, Out, ldo);
+}
+
 static inline size_t combine_smem(int k, int nout) {
   return ((size_t)k * ((nout + 1) & ~1) + 16 + nout) * sizeof(double);
 }
@@ -476,8 +562,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) {
       return st;
     }
-    if (k <= 64) scw_combine_kernel<64, true><<<dim3(nb(n, 256), bc), 128, combine_smem(k, k), s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
-    else scw_combine_kernel<128, true><<<dim3(nb(n, 256), bc), 128, combine_smem(k, k), s>>>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0);
+    launch_combine2<true>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0, bc, s);
+    ctx->count_launch();
     if ((st = launch_status("scw vt")) != TSK_OK) return st;
     // 3. Z^T = V^T A^T
     {
@@ -518,13 +604,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw + (size_t)off * m * ldf;
     float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf + (size_t)off * n * ldf;
-    if (k <= 64) {
-      scw_combine_kernel<64, false><<<dim3(nb(m, 256), bc), 128, combine_smem(k, r), s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
-      scw_combine_kernel<64, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
-    } else {
-      scw_combine_kernel<128, false><<<dim3(nb(m, 256), bc), 128, combine_smem(k, r), s>>>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf);
-      scw_combine_kernel<128, false><<<dim3(nb(n, 256), bc), 128, combine_smem(k, r), s>>>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf);
-    }
+    launch_combine2<false>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf, bc, s);
+    launch_combine2<false>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf, bc, s);
     ctx->count_launch(2);
     if (sigma) {
       scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
