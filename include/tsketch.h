@@ -164,11 +164,21 @@ tsk_status sketch_train(tsk_ctx ctx, const float* A, int64_t D, int m, int n, in
 tsk_status sketch_apply_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
                             float* L, float* R, float* sigma);
 
-/* Per-matrix SCW error err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64, dense residual with an fp64
-   reduction, not ||A||^2 - sum sigma^2).  err: [B] fp64 (device or host).  B = 0 is a no-op and
-   then accepts NULL pointers (as does sketch_apply_scw). */
+/* Per-matrix SCW error err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64).  err: [B] fp64 (device or host).
+   B = 0 is a no-op and then accepts NULL pointers (as does sketch_apply_scw).
+   Formula (tsk_set_scw_error_mode; reading c17): A_hat = [A V]_r V^T is A P with P the
+   orthogonal projector onto span(V W_r), so by default
+     err^2 = ||A||_F^2 - sum_{i<r} sigma_i^2
+   with ||A||_F^2 summed in fp64 while the SA product streams A; where this cancels (err^2 below
+   tau ||A||^2, default tau = 3e-3, e.g. exactly low-rank matrices) the matrix gets the dense residual
+   ||A - L R^T||_F on tcgen05 with an fp64 reduction instead.  Mode 1: the dense residual for all. */
 tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k, int r,
                      double* err);
+
+/* Error formula of scw_error on this ctx: mode 0 = Pythagorean identity with the dense residual below
+   tau ||A||^2 (tau <= 0: the default 3e-3), mode 1 = dense residual for every matrix.  TSK_EINVAL for
+   another mode or tau >= 1 / NaN.  Host-side setting, no GPU work. */
+tsk_status tsk_set_scw_error_mode(tsk_ctx ctx, int mode, double tau);
 
 /* ---------------------------------------------------------------------- two-sided variant */
 /* the paper's second algorithm (Section 3.2).  The

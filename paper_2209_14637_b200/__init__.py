@@ -35,7 +35,7 @@ EXPORTED = ["tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "tsk_stat
             "sketch_gram", "sketch_topk", "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2",
             "sketch_train_two_sided", "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe",
             "tsk_eig_probe", "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init",
-            "tsk_syev_probe", "tsk_allgather_errors", "tsk_allreduce_gram"]
+            "tsk_syev_probe", "tsk_allgather_errors", "tsk_allreduce_gram", "tsk_set_scw_error_mode"]
 
 
 class TskError(RuntimeError):
@@ -120,13 +120,14 @@ def lib() -> ctypes.CDLL:
         L.tsk_syev_probe.argtypes = [vp, f64p, i32, i32, f64p, f64p, vp, ctypes.c_double]
         L.tsk_allgather_errors.argtypes = [vp, f64p, i64, f64p]
         L.tsk_allreduce_gram.argtypes = [vp, f64p, i32]
+        L.tsk_set_scw_error_mode.argtypes = [vp, i32, ctypes.c_double]
         L.sketch_train_matrix_free.argtypes = [vp, f32p, i64, i32, i32, i32, f32p, f64p, vp, vp]
         L.tsk_get_unique_id.argtypes = [vp]
         L.tsk_comm_init.argtypes = [vp, i32, i32, vp]
         for f in ("tsk_create", "tsk_destroy", "tsk_set_stream", "tsk_sync", "sketch_gram", "sketch_topk",
                   "sketch_train", "sketch_apply_scw", "scw_error", "sketch_gram_mode2", "sketch_train_two_sided",
                   "sketch_apply_two_sided_scw", "two_sided_scw_error", "tsk_gram_probe", "tsk_eig_probe", "tsk_syev_probe", "tsk_allgather_errors", "tsk_allreduce_gram",
-                  "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"):
+                  "tsk_set_scw_error_mode", "sketch_train_matrix_free", "tsk_get_unique_id", "tsk_comm_init"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -343,7 +344,7 @@ def sketch_apply_scw(A: torch.Tensor, S: torch.Tensor, r: int, want=("L", "R", "
 
 def scw_error(A: torch.Tensor, S: torch.Tensor, r: int, out: Optional[torch.Tensor] = None,
               ctx: Optional[Context] = None) -> torch.Tensor:
-    """err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64, dense residual)."""
+    """err[b] = ||A_b - SCW(A_b, S, r)||_F (fp64; formula per set_scw_error_mode, include/tsketch.h)."""
     _need(A, torch.float32, "A", 3)
     _need(S, torch.float32, "S", 2)
     B, m, n = A.shape
@@ -352,6 +353,13 @@ def scw_error(A: torch.Tensor, S: torch.Tensor, r: int, out: Optional[torch.Tens
     err = out if out is not None else _alloc((B,), torch.float64, A)
     _check(lib().scw_error(ctx.handle, _ptr(A), B, m, n, _ptr(S), k, r, _ptr(err)), "scw_error")
     return err
+
+
+def set_scw_error_mode(mode: int, tau: float = 0.0, ctx: Optional[Context] = None) -> None:
+    """scw_error's formula on `ctx` (tsk_set_scw_error_mode): 0 = Pythagorean identity with the dense
+    residual below tau ||A||^2 (tau <= 0: library default), 1 = dense residual for every matrix."""
+    ctx = ctx or context()
+    _check(lib().tsk_set_scw_error_mode(ctx.handle, int(mode), float(tau)), "tsk_set_scw_error_mode")
 
 
 def tsk_gram_probe(A: torch.Tensor, mode: int = 0, chain: int = 0, splits: int = 0, G64=None,

@@ -323,6 +323,14 @@ tsk_status tsk_destroy(tsk_ctx ctx) {
   return TSK_OK;
 }
 
+tsk_status tsk_set_scw_error_mode(tsk_ctx ctx, int mode, double tau) {
+  if (!ctx) return TSK_ENULL;
+  if (mode < 0 || mode > 1 || !(tau < 1.0) || tau != tau) return TSK_EINVAL;
+  ctx->c.scw_err_mode = mode;
+  ctx->c.scw_tau = tau > 0.0 ? tau : 0.0;
+  return TSK_OK;
+}
+
 tsk_status tsk_set_stream(tsk_ctx ctx, void* cuda_stream) {
   if (!ctx) return TSK_ENULL;
   Ctx& c = ctx->c;

@@ -69,7 +69,15 @@ struct GemmArgs {
   double* res_part;   // [units][8] (one partial per epilogue warp, fixed order)
   long long dstride;
   int ldd;
+  const int* only;   // batch mode: problems b with only[b] == 0 are skipped by every role (null: all)
+  double* sq_part;   // TS kernel: [U][4] fp64 sums of the squared X elements of each unit (transform warps)
 };
+
+// batch mode with a problem mask: unit u belongs to a skipped problem (same test in every role, so the
+// ring / accumulator phases stay in step)
+__device__ __forceinline__ bool unit_skipped(const GemmArgs& a, int u) {
+  return a.only != nullptr && a.only[(u % a.T) / a.T0] == 0;
+}
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& bi, int& bj) {
   if (a.batch) t %= a.T0;
@@ -374,6 +382,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // TMEM: two 128-column accumulators (double buffer; H H^T and the cross terms share one) + three
 // 64-column A stages [H_X | L_X].  Shared memory: 5 raw TMA stages [X|Y] + 3 lo stages [L_Y].
 constexpr int kTsLoStages = 3;
+// Split rounding (TS kernel): hi(x) = x rounded to nearest tf32 for the X operand (written to TMEM), and
+// lo = x - hi, which then has a random sign: the tensor core truncates its operands, so truncated hi
+// parts leave lo with the sign of x and the dropped lo x lo' and the truncation of lo bias every product
+// toward zero (~3e-7 relative on SCW's AV, which the Pythagorean error reads at first order, reading
+// c17).  Y keeps the hardware-truncated raw tile as hi; its lo part is rounded to nearest.
+constexpr bool kYLoRn = true;
 constexpr int kTsSmemBytes = (kRawStages * 2 + kTsLoStages) * kTileBytes + 1024 + 256;
 constexpr uint32_t kTsAccCols = 128;
 constexpr uint32_t kTsAStageCols = 64;
@@ -441,6 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ybytes = (uint32_t)(a.bn * kBK * 4);
       long long idx = 0;  // CTA-wide chunk index (stage = idx % RS, use = idx / RS)
       for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        if (unit_skipped(a, u)) continue;
         int t, bi, bj;
         long long q0, q1;
         unit_range(a, u, t, q0, q1);
@@ -497,6 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ab = 0;
       uint32_t aph = 0;
       for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+        if (unit_skipped(a, u)) continue;
         int t, bi, bj;
         long long q0, q1;
         unit_range(a, u, t, q0, q1);
@@ -546,11 +562,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int rs = 0, ls = 0;
     uint32_t rph = 0, lph = 0;
     for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      if (unit_skipped(a, u)) continue;
       int t, bi, bj;
       long long q0, q1;
       unit_range(a, u, t, q0, q1);
       tile_coords(a, t, bi, bj);
       const bool diag = a.sym && bi == bj;
+      double sq = 0.0;  // this thread's sum of squared X elements over the unit (a.sq_part)
       for (long long q = q0; q < q1; ++q) {
         mbar_wait(&rfull[rs], rph);
         mbar_wait(&lempty[ls], lph ^ 1);
@@ -564,9 +582,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
               const float e = xcol[c * kBM];
-              const uint32_t h = __float_as_uint(e) & 0xFFFFE000u;
+              const uint32_t h = tf32_rna(e);
               hi[c] = h;
               lo[c] = __float_as_uint(e - __uint_as_float(h));
+            }
+            if (a.sq_part) {  // fp32 within the chunk (32 positive terms), fp64 across chunks
+              float cs = 0.f;
+#pragma unroll
+              for (int c = 0; c < 32; ++c) cs = fmaf(xcol[c * kBM], xcol[c * kBM], cs);
+              sq += (double)cs;
             }
           } else {
             const uint32_t xrow = smem_u32(raw_ptr(rs, 0)) + (uint32_t)tt * 128u;
@@ -576,9 +600,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const uint32_t h = __float_as_uint(e[j]) & 0xFFFFE000u;
+                const uint32_t h = tf32_rna(e[j]);
                 hi[c * 4 + j] = h;
                 lo[c * 4 + j] = __float_as_uint(e[j] - __uint_as_float(h));
+              }
+              if (a.sq_part) {
+                float cs = 0.f;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) cs = fmaf(e[j], e[j], cs);
+                sq += (double)cs;
               }
             }
           }
@@ -604,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float e = ycol[(c * 4 + j) * ys];
                 const float hh = __uint_as_float(__float_as_uint(e) & 0xFFFFE000u);
                 hv[j] = hh;
-                lv[j] = e - hh;
+                lv[j] = __uint_as_float(tf32_rna(e - hh));
               }
               const uint32_t off = (uint32_t)((c ^ (tt & 7)) * 16);
               sts_f4(hrow + off, h);
@@ -619,10 +649,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t off = (uint32_t)(i * 128 + tt) * 16u;
             const float4 v = lds_f4(src + off);
             float4 l;
-            l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-            l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-            l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-            l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            if (kYLoRn) {
+              l.x = __uint_as_float(tf32_rna(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u)));
+              l.y = __uint_as_float(tf32_rna(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u)));
+              l.z = __uint_as_float(tf32_rna(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u)));
+              l.w = __uint_as_float(tf32_rna(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u)));
+            } else {
+              l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+              l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+              l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+              l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+            }
             sts_f4(dst + off, l);
           }
         }
@@ -634,17 +671,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++rs == RS) { rs = 0; rph ^= 1; }
         if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
       }
+      if (a.sq_part) {  // fixed-order warp reduction: one partial per (unit, transform warp)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) a.sq_part[(size_t)u * 4 + quad] = sq;
+      }
     }
   } else if (warp >= 8) {
     // ===================== epilogue: TMEM chains -> fp32 registers -> fp64 partials =====================
     const int e = warp - 8;
     const int quad = warp & 3;
-    const int col0 = (e >> 2) * 64;
+    // columns per epilogue warp: 64 of the 128-wide accumulator, or 32 of a 64-wide output (N = 64:
+    // both warp groups drain, and a thread holds 32 + 2 x 32 values instead of 64 + 2 x 32 -- no spills)
+    constexpr int kEC = kN64 ? 32 : 64;
+    const int col0 = (e >> 2) * kEC;
     const int row = quad * 32 + lane;
     int ab = 0;
     uint32_t aph = 0;
     const bool has_cols = col0 < a.bn;
     for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
+      if (unit_skipped(a, u)) continue;
       int t;
       long long q0, q1;
       unit_range(a, u, t, q0, q1);
@@ -678,6 +724,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&accf[ab], aph);
           tc_fence_after();
           const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)ab * kTsAccCols + col0;
+          // (a - s)^2 in fp32 (the difference is exact or correctly rounded, a 32-term sum of squares
+          // carries ~1e-7 relative rounding), fp64 across halves and units: the fp64 version spent
+          // ~70 % of the epilogue in F2F.F64 conversions
           double acc = 0.0;
           if (has_cols) {
 #pragma unroll
@@ -685,13 +734,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t r[32];
               tmem_ld_32x32b_x32(taddr + h * 32, r);
               tmem_ld_wait();
+              float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                if (h * 32 + i < nv) {
-                  const double d = (double)av[h * 32 + i] - (double)__uint_as_float(r[i]);
-                  acc += d * d;
-                }
+              for (int i = 0; i < 32; i += 2) {
+                const float d0 = (h * 32 + i < nv) ? av[h * 32 + i] - __uint_as_float(r[i]) : 0.f;
+                const float d1 = (h * 32 + i + 1 < nv) ? av[h * 32 + i + 1] - __uint_as_float(r[i + 1]) : 0.f;
+                s0 = fmaf(d0, d0, s0);
+                s1 = fmaf(d1, d1, s1);
               }
+              acc += (double)s0 + (double)s1;
             }
           }
           tc_fence_before();
@@ -704,9 +755,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
       }
-      float sum[64];
+      float sum[kEC];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+      for (int i = 0; i < kEC; ++i) sum[i] = 0.f;
       // staggered folds: epilogue warp e folds (fp32 -> fp64 reductions at L2) at chains offset by
       // e * fold / 8, so no single accumulator drain carries all the L2 reductions of a fold
       int cin = (e * a.fold) / 8;
@@ -718,19 +769,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)ab * kTsAccCols + col0;
         if (has_cols) {
           if constexpr (kN64) {  // separate accumulators: columns [0,64) = H H^T, [64,128) = cross terms
+            uint32_t r[32], x[32];
+            tmem_ld_32x32b_x32(taddr, r);
+            tmem_ld_32x32b_x32(taddr + 64, x);
+            tmem_ld_wait();
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              uint32_t r[32];
-              tmem_ld_32x32b_x32(taddr + h * 32, r);
-              tmem_ld_wait();
-              float t[32];
-#pragma unroll
-              for (int i = 0; i < 32; ++i) t[i] = __uint_as_float(r[i]);
-              tmem_ld_32x32b_x32(taddr + 64 + h * 32, r);
-              tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) sum[h * 32 + i] += t[i] + __uint_as_float(r[i]);
-            }
+            for (int i = 0; i < 32; ++i) sum[i] += __uint_as_float(r[i]) + __uint_as_float(x[i]);
           } else {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -751,14 +795,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t pol = l2_policy_evict_last();
           if (first_fold) {
 #pragma unroll
-            for (int i = 0; i < 64; i += 2)
+            for (int i = 0; i < kEC; i += 2)
               st_f64x2_hint(reinterpret_cast<double2*>(prow + i), make_double2((double)sum[i], (double)sum[i + 1]), pol);
           } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) red_add_f64_hint(prow + i, (double)sum[i], pol);
+            for (int i = 0; i < kEC; ++i) red_add_f64_hint(prow + i, (double)sum[i], pol);
           }
 #pragma unroll
-          for (int i = 0; i < 64; ++i) sum[i] = 0.f;
+          for (int i = 0; i < kEC; ++i) sum[i] = 0.f;
           first_fold = false;
           cin = 0;
         }
@@ -773,10 +817,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         double acc = 0.0;
         if (has_cols && gr < a.Mv) {
           const float* ar = a.resA + (size_t)b * a.res_stride + (size_t)gr * a.res_ld + (size_t)bj * a.bn + col0;
-          const int nv = min(64, min(a.bn - col0, a.Nv - (bj * a.bn + col0)));
-          if (nv == 64 && ((reinterpret_cast<uintptr_t>(ar) & 15) == 0)) {
+          const int nv = min(kEC, min(a.bn - col0, a.Nv - (bj * a.bn + col0)));
+          if (nv == kEC && ((reinterpret_cast<uintptr_t>(ar) & 15) == 0)) {
 #pragma unroll
-            for (int i = 0; i < 64; i += 4) {
+            for (int i = 0; i < kEC; i += 4) {
               const float4 v = __ldg(reinterpret_cast<const float4*>(ar + i));
               const double d0 = (double)v.x - (double)sum[i], d1 = (double)v.y - (double)sum[i + 1];
               const double d2 = (double)v.z - (double)sum[i + 2], d3 = (double)v.w - (double)sum[i + 3];
@@ -784,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) {
+            for (int i = 0; i < kEC; ++i) {
               if (i < nv) {
                 const double d = (double)__ldg(ar + i) - (double)sum[i];
                 acc += d * d;
@@ -822,13 +866,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (gr < a.Mv) {
           if (a.drow) {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) {
+            for (int i = 0; i < kEC; ++i) {
               const int gc = bj * a.bn + col0 + i;
               if (col0 + i < a.bn && gc < a.Nv) ob[(size_t)gr * a.ldd + gc] = sum[i];
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i) {
+            for (int i = 0; i < kEC; ++i) {
               const int gc = bj * a.bn + col0 + i;
               if (col0 + i < a.bn && gc < a.Nv) ob[(size_t)gc * a.ldd + gr] = sum[i];
             }
@@ -998,6 +1042,9 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.res_stride = p.res_stride;
   a.res_ld = p.res_ld;
   a.res_part = p.res_part;
+  a.only = p.only;
+  a.sq_part = p.sq_part;
+  if ((p.only || p.sq_part) && !p.batch) return TSK_EINVAL;
   a.dout = p.dout;
   a.dstride = p.dstride;
   a.ldd = p.ldd;

@@ -193,15 +193,17 @@ static void launch_jacobi(int batch, int threads, size_t smem, cudaStream_t st, 
   jacobi_eig_kernel<kSmem, NQ, KQ><<<batch, threads, smem, st>>>(H, p, W, lam, scratch, 30, tol, sweeps, gate);
 }
 
+long long jacobi_ws_doubles(int p) { return (long long)2 * p * (p + 1); }
+
 tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam, int* sweeps,
-                              double tol, const int* gate) {
+                              double tol, const int* gate, double* scratch_ext) {
   if (p < 1 || p > 256 || batch < 0) return TSK_EINVAL;
   if (batch == 0) return TSK_OK;
-  const size_t need = (size_t)2 * p * (p + 1) * sizeof(double);
+  const size_t need = (size_t)jacobi_ws_doubles(p) * sizeof(double);
   int use_smem = need <= (size_t)kJacSmemMax;
   double* scratch = nullptr;
   if (!use_smem) {
-    scratch = reinterpret_cast<double*>(ctx->workspace(WS_JACOBI, need * batch));
+    scratch = scratch_ext ? scratch_ext : reinterpret_cast<double*>(ctx->workspace(WS_JACOBI, need * batch));
     if (!scratch) return TSK_ENOMEM;
   }
   const size_t smem = use_smem ? need : 0;

@@ -195,15 +195,44 @@ __global__ void scw_sigma_kernel(const double* __restrict__ sig2, int k, int r, 
 
 // err[b] = sqrt(sum of the b-th matrix's residual partials): one warp per matrix, lanes strided, fixed-
 // order butterfly (deterministic)
-__global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles, long long B, double* __restrict__ err) {
+// (only: matrices with only[b] == 0 keep their error -- they were not part of the residual launch)
+__global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles, long long B, double* __restrict__ err,
+                                      const int* __restrict__ only) {
   const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
+  if (only && only[b] == 0) return;
   double s = 0.0;
   for (int t = lane; t < tiles; t += 32) s += part[b * tiles + t];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) err[b] = sqrt(s);
+}
+
+// err_b by the Pythagorean identity (reading c17): Algorithm 1's A_hat = [AV]_r V^T
+// is A P with P = (V W_r)(V W_r)^T an orthogonal projector (V orthonormal, W_r the top-r
+// eigenvectors of (AV)^T AV), so ||A - A_hat||_F^2 = ||A||_F^2 - ||A V W_r||_F^2 = ||A||_F^2 -
+// sum_{i<r} sigma_i^2.  ||A||_F^2 comes from the SA product's transform warps (sq partials, fp64, fixed
+// order), sigma_i^2 are the eigenvalues of (AV)^T AV.  The subtraction cancels when the error is small
+// against ||A||: below tau ||A||^2 (or a non-finite value) the matrix is marked for the dense residual
+// ||A - L R^T|| (dense[b] = 1), which then overwrites err[b].  One warp per matrix, fixed-order sums.
+__global__ void scw_err_pyth_kernel(const double* __restrict__ sq, int per, const double* __restrict__ sig2, int k,
+                                    int r, long long B, double tau, double* __restrict__ err, int* __restrict__ dense) {
+  const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int t = lane; t < per; t += 32) s += sq[b * per + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    double kept = 0.0;
+    for (int i = 0; i < r; ++i) kept += fmax(sig2[b * k + i], 0.0);
+    const double e2 = s - kept;
+    const bool need = !(e2 >= tau * s) || !(s < INFINITY);
+    err[b] = need ? 0.0 : sqrt(e2);
+    dense[b] = need ? 1 : 0;
+  }
 }
 
 // ---------------------------------------------------------------- C = X X^T, register-tiled fp64
@@ -425,6 +454,9 @@ __global__ void __launch_bounds__(128) chol_basis_kernel(const double* __restric
   for (int c = tid; c < k; c += nt) mu[(size_t)b * k + c] = c < rk ? 1.0 : 0.0;
 }
 
+// below err^2 = tau ||A||^2 the Pythagorean error is replaced by the dense residual (reading c17)
+constexpr double kScwPythTau = 3e-3;
+
 static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 
@@ -432,7 +464,7 @@ static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / 
 // (3xTF32, K = r, one 128 x 128 tile per unit) with the residual epilogue of gemm_tc.cu reading
 // the A tile and reducing (a - s)^2 in fp64; fixed-order reduction of the per-warp partials.
 static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, const float* Lc, const float* Rc,
-                              int r, int ldf, double* part, double* err) {
+                              int r, int ldf, double* part, double* err, const int* only = nullptr) {
   GemmProblem gp;
   gp.X = Lc;
   gp.Y = Rc;
@@ -450,10 +482,11 @@ static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, c
   gp.res_stride = (long long)m * n;
   gp.res_ld = n;
   gp.res_part = part;
+  gp.only = only;
   tsk_status st = gemm_tf32x3(ctx, gp);
   if (st != TSK_OK) return st;
   const int per = (int)(nb(m, 128) * nb(n, 128)) * 8;  // partials per matrix
-  scw_err_reduce_kernel<<<nb((long long)bc * 32, 256), 256, 0, ctx->stream>>>(part, per, bc, err);
+  scw_err_reduce_kernel<<<nb((long long)bc * 32, 256), 256, 0, ctx->stream>>>(part, per, bc, err, only);
   ctx->count_launch();
   return launch_status("scw residual (tcgen05)");
 }
@@ -486,8 +519,23 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   // factor row pitch: r for the caller's L / R, r rounded up to 4 (16-byte TMA rows) for the error path
   const int ldf = (L || R) ? r : (r + 3) & ~3;
   float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * ldf * 4));
-  double* part = reinterpret_cast<double*>(ctx->workspace(WS_SCW_5, chunk * (size_t)tiles * 8 + 64));
+  // residual partials, then the ||A||^2 partials of the SA product (4 per unit, nb(n, 128) units per
+  // matrix) and the dense-residual marks of the Pythagorean error path
+  const int sq_per = (int)nb(n, 128) * 4;
+  double* part = reinterpret_cast<double*>(
+      ctx->workspace(WS_SCW_5, chunk * ((size_t)tiles + sq_per) * 8 + chunk * 4 + 64));
   if (!Bm_all || !Vt_all || !Zt_all || !small || !Lw || !part) return TSK_ENOMEM;
+  double* sq_all = part + chunk * tiles;
+  // eigensolver scratch per matrix: the parts run concurrently on different streams
+  const long long eig_ws = std::max(syev_ws_doubles(k), jacobi_ws_doubles(k));
+  double* eigws_all = reinterpret_cast<double*>(ctx->workspace(WS_SCW_EIG, (size_t)chunk * eig_ws * 8));
+  if (!eigws_all) return TSK_ENOMEM;
+  int* dense_all = reinterpret_cast<int*>(sq_all + chunk * sq_per);
+  // Pythagorean error path (reading c17) unless TSK_SCW_DENSE; tau: the cancellation threshold
+  static const bool force_dense = getenv("TSK_SCW_DENSE") != nullptr;
+  static const double env_tau = getenv("TSK_SCW_PYTH_TAU") ? atof(getenv("TSK_SCW_PYTH_TAU")) : kScwPythTau;
+  const double pyth_tau = ctx->scw_tau > 0.0 ? ctx->scw_tau : env_tau;
+  const bool pyth = err && !force_dense && ctx->scw_err_mode == 0;
   double* Cb_all = small;
   double* Wc_all = small + chunk * kk;
   double* H_all = small + 2 * chunk * kk;
@@ -525,6 +573,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     double* W2 = W2_all + off * kk;
     double* mu = mu_all + off * k;
     double* sig2 = sig2_all + off * k;
+    double* eigws = eigws_all + off * eig_ws;
     // 1. B = S A on tcgen05 (3xTF32): (S A_b)^T = A_b^T S^T with X = A_b read transposed (the
     // contraction runs over the rows of A_b), Y = S broadcast to every matrix; one unit per
     // (matrix, 128-column tile of A_b), stored transposed as B [k][n]
@@ -547,6 +596,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       gp.dout = Bm;
       gp.dstride = (long long)k * n;
       gp.ldd = n;
+      if (pyth) gp.sq_part = sq_all + off * sq_per;
       if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
     }
     if (after_sa) cudaEventRecord(after_sa, s);
@@ -559,7 +609,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cb, k, Wc, mu);
       ctx->count_launch(1);
       if ((st = launch_status("scw chol_basis")) != TSK_OK) return st;
-    } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10)) != TSK_OK) {
+    } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10, nullptr, eigws)) != TSK_OK) {
       return st;
     }
     launch_combine2<true>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0, bc, s);
@@ -585,6 +635,11 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       gp.dout = Zt;
       gp.dstride = (long long)k * m;
       gp.ldd = m;
+      // the Pythagorean error is first-order in a scale bias of AV: one TMEM accumulation chain per
+      // 32-deep chunk (the tensor core's truncating accumulation, reading c17), fp32 sums across chunks;
+      // the same on the dense error path, so both formulas see the same factors
+      static const int av_chain = getenv("TSK_SCW_AV_CHAIN") ? atoi(getenv("TSK_SCW_AV_CHAIN")) : 0;
+      gp.chain = av_chain > 0 ? av_chain : (err ? 1 : 0);
       if ((st = gemm_tf32x3(ctx, gp)) != TSK_OK) return st;
     }
     // 4. SVD of AV through its Gram
@@ -598,8 +653,8 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     {
       int* gflag = reinterpret_cast<int*>(small + chunk * (4 * kk + 2 * k)) + off;
       cudaMemsetAsync(gflag, 0, sizeof(int), s);
-      if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k)) != TSK_OK) return st;
-      if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag)) != TSK_OK) return st;
+      if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k, eigws)) != TSK_OK) return st;
+      if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag, eigws)) != TSK_OK) return st;
     }
     // 5. factors
     float* Lc = L ? L + (size_t)b0 * m * r : Lw + (size_t)off * m * ldf;
@@ -611,8 +666,16 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
       ctx->count_launch();
     }
-    // 6. dense residual (the error path always has pitch-aligned workspace factors)
-    if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part + (size_t)off * tiles, err + b0)) != TSK_OK) return st;
+    // 6. errors: Pythagorean identity, dense residual for the marked matrices (all of them with
+    // TSK_SCW_DENSE); the error path always has pitch-aligned workspace factors
+    if (pyth) {
+      scw_err_pyth_kernel<<<nb((long long)bc * 32, 256), 256, 0, s>>>(sq_all + off * sq_per, sq_per, sig2, k, r, bc,
+                                                                      pyth_tau, err + b0, dense_all + off);
+      ctx->count_launch();
+    }
+    if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part + (size_t)off * tiles, err + b0,
+                                 pyth ? dense_all + off : nullptr)) != TSK_OK)
+      return st;
     if ((st = launch_status("scw")) != TSK_OK) return st;
     return TSK_OK;
   };

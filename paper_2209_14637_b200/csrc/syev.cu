@@ -952,16 +952,21 @@ __global__ void __launch_bounds__(512) orth_kernel(const double* __restrict__ W,
 }
 
 // batch of problems: H [batch][p][p], W [batch][p][ldw] (stride p * ldw), lam [batch][nw]
+// per-problem workspace: refl [p][p], A scratch [p][p] (p > 160), tau, d, e [p] each
+long long syev_ws_doubles(int p) {
+  const size_t pp = (size_t)p * p;
+  return (long long)((pp * 2 + 3 * (size_t)p + 16 + 1) & ~(size_t)1);  // even: 16-B aligned
+}
+
 tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch, double* W, int ldw, double* lam,
-                            int* flag, double orth_tol, long long lstride) {
+                            int* flag, double orth_tol, long long lstride, double* ws) {
   if (p < 1 || p > 256 || nw < 1 || nw > p || ldw < nw || batch < 0) return TSK_EINVAL;
   if (lstride <= 0) lstride = nw;
   if (batch == 0) return TSK_OK;
   cudaStream_t st = ctx->stream;
-  // per-problem workspace: refl [p][p], A scratch [p][p] (p > 160), tau, d, e [p] each
   const size_t pp = (size_t)p * p;
-  const long long wsz = (long long)((pp * 2 + 3 * (size_t)p + 16 + 1) & ~(size_t)1);  // even: 16-B aligned
-  double* ws = reinterpret_cast<double*>(ctx->workspace(WS_SYEV, (size_t)wsz * batch * sizeof(double)));
+  const long long wsz = syev_ws_doubles(p);
+  if (!ws) ws = reinterpret_cast<double*>(ctx->workspace(WS_SYEV, (size_t)wsz * batch * sizeof(double)));
   if (!ws) return TSK_ENOMEM;
   double* refl = ws;
   double* gA = ws + pp;

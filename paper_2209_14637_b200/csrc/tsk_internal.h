@@ -69,6 +69,7 @@ enum WorkspaceId {
   WS_EIG_GQ,       // eigensolver: split-K partial tiles + tickets of the fp64 product
   WS_SYEV,         // small symmetric eigensolver: reflectors, tridiagonal, scratch
   WS_GATHER,       // tsk_allgather_errors: padded [P][per] gather buffer
+  WS_SCW_EIG,    // per-part eigensolver scratch of the batched SCW (its parts run concurrently)
   WS_COUNT
 };
 
@@ -120,6 +121,10 @@ struct Ctx {
     return host_pinned;
   }
   void count_launch(int n = 1) { launches += n; }
+  // scw_error's error formula (tsk_set_scw_error_mode): 0 = Pythagorean identity with the dense
+  // residual below tau ||A||^2 (tau <= 0: the library default), 1 = dense residual for every matrix
+  int scw_err_mode = 0;
+  double scw_tau = 0.0;
   // NCCL communicator of tsk_comm_init (ncclComm_t, opaque here; nullptr = single GPU)
   void* comm = nullptr;
   int nranks = 1, rank = 0;
@@ -186,6 +191,12 @@ struct GemmProblem {
   long long res_stride = 0;
   int res_ld = 0;
   double* res_part = nullptr;
+  // batch mode: only problems b with only[b] != 0 are computed (the others' outputs are not written)
+  const int* only = nullptr;
+  // TS kernel, batch mode: sq_part[unit][4] = fp64 sums of the squared X elements each unit reads
+  // (unit u of problem b: u = b * tiles + tile; every X element of a problem in exactly one unit when N
+  // fits one column block)
+  double* sq_part = nullptr;
   int bn = 128;           // MMA N tile: 128 or 64
   float* dout = nullptr;  // direct fp32 output, transposed: dout[b * dstride + col * ldd + row]
   long long dstride = 0;
@@ -225,16 +236,23 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
 tsk_status syev_top(Ctx* ctx, const double* H, int p, int nw, double* W, int ldw, double* lam, int* flag,
                     double orth_tol);
 // the same for a batch: H [batch][p][p], W [batch][p][ldw], lam [batch][nw]; flag set if any problem fails
+// ws (optional): caller-owned scratch of syev_ws_doubles(p) doubles per problem (else the ctx's WS_SYEV,
+// which two concurrent calls on different streams must not share)
 tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch, double* W, int ldw, double* lam,
-                            int* flag, double orth_tol, long long lstride = 0);
+                            int* flag, double orth_tol, long long lstride = 0, double* ws = nullptr);
+long long syev_ws_doubles(int p);
 
 // batched symmetric PSD eigensolver (one-sided Jacobi), jacobi.cu
 // H: [batch][p][p] fp64 symmetric (row-major, read only).  W: [batch][p][p] fp64 eigenvectors as
 // COLUMNS (W[b][i][c] = component i of eigenvector c), lam: [batch][p] fp64 decreasing.
 // gate (device int, may be null): the kernel returns at once unless *gate != 0 (a device-side fallback
 // behind syev_top_batched's orthogonality flag, no host round trip)
+// scratch (optional): caller-owned, jacobi_ws_doubles(p) doubles per problem (used only for p where the
+// matrix pair does not fit shared memory; else the ctx's WS_JACOBI)
 tsk_status jacobi_eig_batched(Ctx* ctx, const double* H, int p, int batch, double* W, double* lam,
-                              int* sweeps = nullptr, double tol = 1e-13, const int* gate = nullptr);
+                              int* sweeps = nullptr, double tol = 1e-13, const int* gate = nullptr,
+                              double* scratch = nullptr);
+long long jacobi_ws_doubles(int p);
 
 }  // namespace tsk
 

@@ -71,6 +71,8 @@ def test_null_and_argument_errors_without_gpu(lib):
     assert lib.sketch_train(None, vp(1), 1, 4, 4, 2, vp(1), None, None, None, None) == -8
     assert lib.sketch_apply_scw(None, vp(1), 1, 4, 4, vp(1), 2, 1, None, None, None) == -8
     assert lib.scw_error(None, vp(1), 1, 4, 4, vp(1), 2, 1, vp(1)) == -8
+    lib.tsk_set_scw_error_mode.argtypes = [vp, ctypes.c_int, ctypes.c_double]
+    assert lib.tsk_set_scw_error_mode(None, 0, 0.0) == -8
     assert lib.tsk_create(None, 0, None) == -8
     # no sm_100 device here: tsk_create reports TSK_EDEVICE instead of falling back to the CPU
     h = ctypes.c_void_p()

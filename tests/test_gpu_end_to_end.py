@@ -65,9 +65,13 @@ def test_algorithm2_end_to_end(cfg, ntest):
     e_o = oscw.scw_errors(Tn, S_o, c.r)
     fro = np.linalg.norm(Tn.reshape(Tn.shape[0], -1).astype(np.float64), axis=1)
     assert np.all(np.abs(e - e_o) <= 1e-4 * e_o + 1e-6 * fro), np.max(np.abs(e - e_o) / e_o)
-    # the paper's test-error metric over the sample, GPU vs oracle
+    # the paper's test-error metric over the sample, GPU vs oracle: mean_b (e_b - eopt_b) / eopt_b
+    # moves by at most mean_b |e_b - e_o,b| / eopt_b, so the per-matrix bound above (1e-4 e_o + 1e-6 ||A||,
+    # BASELINE.json) bounds it -- the metric is a difference of nearly equal errors (~1e-4 at C1), so a
+    # relative tolerance on it would ask ~1e-7 of each error, which BASELINE does not
     eopt = np.array([oscw.best_rank_r_error(a, c.r) for a in Tn])
-    assert oscw.test_error(e, eopt)[0] == pytest.approx(oscw.test_error(e_o, eopt)[0], rel=1e-3, abs=1e-7)
+    bound = np.mean((1e-4 * e_o + 1e-6 * fro) / eopt)
+    assert abs(oscw.test_error(e, eopt)[0] - oscw.test_error(e_o, eopt)[0]) <= bound
 
 
 @pytest.mark.parametrize("cfg,nsample", [("C3", 6), ("C4", 4)])
@@ -107,3 +111,27 @@ def test_two_sided_end_to_end(cfg, k, l, D, ntest):
     e_o = tucker2.two_sided_scw_errors(T.numpy(), So, Wo, r)
     fro = np.linalg.norm(T.numpy().reshape(T.shape[0], -1).astype(np.float64), axis=1)
     assert np.all(np.abs(e - e_o) <= 1e-4 * e_o + 1e-6 * fro), np.max(np.abs(e - e_o) / e_o)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
+def test_scw_error_formulas_agree(cfg):
+    """scw_error's Pythagorean error (mode 0, reading c17) against its dense residual (mode 1) on the same
+    stream and sketch: both are Algorithm 1's ||A - [AV]_r V^T||_F, so they agree within the
+    per-matrix BASELINE tolerance; the dense residual also takes over below tau ||A||^2 (forced here with
+    tau = 0.999: every matrix then goes through the fallback, which must equal mode 1 bit for bit)."""
+    c = datagen.CONFIGS[cfg]
+    T = datagen.generate(c, "test", 0, min(c.D_test, 64), device="cuda")
+    q, _ = np.linalg.qr(np.random.default_rng(3).standard_normal((c.m, c.k)))
+    S = torch.tensor(q.T.copy(), dtype=torch.float32, device="cuda")
+    try:
+        tsk.set_scw_error_mode(1)
+        e_d = tsk.scw_error(T, S, c.r).cpu().numpy()
+        tsk.set_scw_error_mode(0, 0.999)
+        e_f = tsk.scw_error(T, S, c.r).cpu().numpy()
+        tsk.set_scw_error_mode(0)
+        e_p = tsk.scw_error(T, S, c.r).cpu().numpy()
+    finally:
+        tsk.set_scw_error_mode(0)
+    fro = np.linalg.norm(T.cpu().numpy().reshape(T.shape[0], -1).astype(np.float64), axis=1)
+    assert np.all(np.abs(e_p - e_d) <= 1e-4 * e_d + 1e-6 * fro), np.max(np.abs(e_p - e_d) / e_d)
+    np.testing.assert_array_equal(e_f, e_d)

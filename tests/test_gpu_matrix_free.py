@@ -138,7 +138,10 @@ def test_matrix_free_c4_scale():
     assert st == 0 and info["width"] == 192 and info["passes"] == 5
     lam0 = lam0.cpu().numpy()
     lam = lam.cpu().numpy()
-    assert np.all(lam <= lam0 * (1 + 1e-6))
+    # interlacing (exact arithmetic) up to the precision of the compared values: lam0 comes from the 3xTF32
+    # Gram, which BASELINE bounds at 1e-5 relative (its truncating split biases it low by ~1e-6, while the
+    # Krylov products round to nearest)
+    assert np.all(lam <= lam0 * (1 + 1e-5))
     assert lam.sum() >= lam0.sum() * (1 - 1e-2)
     e0 = tsk.scw_error(T, S0, c.r).cpu().numpy()
     e1 = tsk.scw_error(T, S, c.r).cpu().numpy()
