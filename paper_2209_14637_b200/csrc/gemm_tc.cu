@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
               const float e = xcol[c * kBM];
-              const uint32_t h = tf32_rna(e);
+              const uint32_t h = tf32_rn(e);
               hi[c] = h;
               lo[c] = __float_as_uint(e - __uint_as_float(h));
             }
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const uint32_t h = tf32_rna(e[j]);
+                const uint32_t h = tf32_rn(e[j]);
                 hi[c * 4 + j] = h;
                 lo[c * 4 + j] = __float_as_uint(e[j] - __uint_as_float(h));
               }
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float e = ycol[(c * 4 + j) * ys];
                 const float hh = __uint_as_float(__float_as_uint(e) & 0xFFFFE000u);
                 hv[j] = hh;
-                lv[j] = __uint_as_float(tf32_rna(e - hh));
+                lv[j] = __uint_as_float(tf32_rn(e - hh));
               }
               const uint32_t off = (uint32_t)((c ^ (tt & 7)) * 16);
               sts_f4(hrow + off, h);
@@ -650,10 +650,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4 v = lds_f4(src + off);
             float4 l;
             if (kYLoRn) {
-              l.x = __uint_as_float(tf32_rna(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u)));
-              l.y = __uint_as_float(tf32_rna(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u)));
-              l.z = __uint_as_float(tf32_rna(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u)));
-              l.w = __uint_as_float(tf32_rna(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u)));
+              l.x = __uint_as_float(tf32_rn(v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u)));
+              l.y = __uint_as_float(tf32_rn(v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u)));
+              l.z = __uint_as_float(tf32_rn(v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u)));
+              l.w = __uint_as_float(tf32_rn(v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u)));
             } else {
               l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
               l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);

@@ -75,11 +75,14 @@ TSK_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t
 }
 TSK_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// fp32 -> tf32 rounded to nearest (ties away from zero), as the 32-bit pattern the MMA reads (low 13 bits
-// zero): the magnitude bits are rounded in integer arithmetic (sign-magnitude format; a carry into the
-// exponent is the correct rounding).  Finite inputs below 2^128 (1 - 2^-12) only -- cvt.rna.tf32.f32
-// handles Inf / NaN too, but compiles to a branchy sequence that cost ~10 % of the SCW products.
-TSK_DEV uint32_t tf32_rna(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
+// fp32 -> tf32 rounded to nearest even, as the 32-bit pattern the MMA reads (low 13 bits zero):
+// cvt.rn.tf32.f32 is one F2FP.TF32.F32 instruction on sm_100a (cvt.rna compiles to a compare-and-
+// branch sequence, an integer add-and-mask to two ALU ops; the split transform is issue-bound).
+TSK_DEV uint32_t tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
 
 // ---------------------------------------------------------------- Ampere-style async copies + fp64 MMA
 // 8-byte cp.async global -> shared; src_bytes 0 zero-fills the destination (out-of-range element)
