@@ -181,8 +181,10 @@ tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const
 tsk_status tsk_set_scw_error_mode(tsk_ctx ctx, int mode, double tau);
 
 /* ---------------------------------------------------------------------- two-sided variant */
-/* the paper's second algorithm (Section 3.2).  The
-   two-sided entry points take DEVICE pointers only (TSK_EINVAL for host memory). */
+/* the paper's second algorithm (Section 3.2).  Pointers
+   may be host or device memory: host arrays are staged whole into device workspace (copied in, outputs
+   copied back) and the call returns synchronised, as the one-sided host path; device arrays are used in
+   place (fp32 arrays 16-byte aligned, else TSK_ESHAPE). */
 
 /* Mode-2 Gram (the HOSVD initial factor of Algorithm 5 along mode 2):
      G2 (+)= sum_{d<D} A_d^T A_d          A: [D][m][n] fp32 (m % 4 == 0);  G64: [n][n] fp64
@@ -220,15 +222,15 @@ tsk_status sketch_train_two_sided(tsk_ctx ctx, const float* A, int64_t D, int m,
 tsk_status sketch_apply_two_sided_scw(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
                                       const float* W, int l, int r, float* L, float* R, float* sigma);
 
-/* err[b] = ||A_b - two-sided SCW(A_b, S, W, r)||_F (fp64 dense residual), err [B] fp64 device. */
+/* err[b] = ||A_b - two-sided SCW(A_b, S, W, r)||_F (fp64 dense residual), err [B] fp64. */
 tsk_status two_sided_scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
                                const float* W, int l, int r, double* err);
 
 /* ---------------------------------------------------------------------- matrix-free sketch */
 /* the Tucker1 sketch approximated by randomized block
    Krylov on A_(1) without forming the m x m Gram -- the pass-efficient direction the paper names as
-   future work.  Not the paper's algorithm: readings mf1-mf4 in DESIGN.md.  DEVICE pointers
-   only (TSK_EINVAL for host memory).
+   future work.  Not the paper's algorithm: readings mf1-mf4 in DESIGN.md.  Host or device
+   pointers (host arrays staged whole, synchronous; as the two-sided entry points).
      Q_0 = orth(Omega);  for j = 1..q: Y_j = sum_d A_d (A_d^T Q_{j-1}),
        Krylov (default): Y_j -= sum_{i<j} Q_i Q_i^T Y_j (twice), Q_j = orth(Y_j), K = [Q_0|...|Q_q]
        subspace:         Q_j = orth(Y_j), K = Q_q
@@ -244,7 +246,7 @@ typedef struct {
                            default (<= 0): 16 */
   int power_iters;      /* q >= 0; default (< 0): the largest q <= 2 with width <= min(m, 256) */
   int subspace;         /* 1: plain subspace iteration (K = Q_q); 0 (default): block Krylov */
-  const double* omega;  /* optional DEVICE [m][p] fp64 start block (p as above); NULL = deterministic
+  const double* omega;  /* optional [m][p] fp64 start block (p as above; host or device); NULL = deterministic
                            pseudo-random uniform(-1, 1) block */
 } tsk_mf_opts;
 

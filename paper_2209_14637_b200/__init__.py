@@ -409,8 +409,8 @@ def sketch_gram_mode2(A: torch.Tensor, G64: Optional[torch.Tensor] = None, accum
     """G2 (+)= sum_d A_d^T A_d (n x n fp64), the mode-2 Gram (HOSVD init of Algorithm 5)."""
     _need(A, torch.float32, "A", 3)
     D, m, n = A.shape
-    ctx = ctx or context(A.device)
-    G64 = G64 if G64 is not None else torch.empty((n, n), dtype=torch.float64, device=A.device)
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    G64 = G64 if G64 is not None else _alloc((n, n), torch.float64, A)
     _check(lib().sketch_gram_mode2(ctx.handle, _ptr(A), D, m, n, _ptr(G64), int(accumulate)), "sketch_gram_mode2")
     return G64
 
@@ -420,9 +420,9 @@ def sketch_train_two_sided(A: torch.Tensor, k: int, l: int, max_sweeps: int = 0,
     """Tucker2 by HOOI over modes 1-2 (Eq. (9), Algorithm 5): returns (S [k][m], W [l][n], info dict, status)."""
     _need(A, torch.float32, "A", 3)
     D, m, n = A.shape
-    ctx = ctx or context(A.device)
-    S = torch.empty((k, m), dtype=torch.float32, device=A.device)
-    W = torch.empty((l, n), dtype=torch.float32, device=A.device)
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    S = _alloc((k, m), torch.float32, A)
+    W = _alloc((l, n), torch.float32, A)
     o = HooiOpts(max_sweeps, rel_tol)
     info = HooiInfo()
     st = _check(lib().sketch_train_two_sided(ctx.handle, _ptr(A), D, m, n, k, l, _ptr(S), _ptr(W), ctypes.byref(o),
@@ -439,7 +439,7 @@ def sketch_apply_two_sided_scw(A: torch.Tensor, S: torch.Tensor, W: torch.Tensor
     B, m, n = A.shape
     k, l = S.shape[0], W.shape[0]
     rr = min(r, k, l)
-    ctx = ctx or context(A.device)
+    ctx = ctx or context(A.device if A.is_cuda else None)
     L = _alloc((B, m, rr), torch.float32, A)
     R = _alloc((B, n, rr), torch.float32, A)
     sig = _alloc((B, rr), torch.float32, A)
@@ -455,7 +455,7 @@ def two_sided_scw_error(A: torch.Tensor, S: torch.Tensor, W: torch.Tensor, r: in
     _need(S, torch.float32, "S", 2)
     _need(W, torch.float32, "W", 2)
     B, m, n = A.shape
-    ctx = ctx or context(A.device)
+    ctx = ctx or context(A.device if A.is_cuda else None)
     err = _alloc((B,), torch.float64, A)
     _check(lib().two_sided_scw_error(ctx.handle, _ptr(A), B, m, n, _ptr(S), S.shape[0], _ptr(W), W.shape[0], r,
                                      _ptr(err)), "two_sided_scw_error")
@@ -470,9 +470,9 @@ def sketch_train_matrix_free(A: torch.Tensor, k: int, oversample: int = 0, power
     p = k + oversample rounded up to a multiple of 4 (capped at m)."""
     _need(A, torch.float32, "A", 3)
     D, m, n = A.shape
-    ctx = ctx or context(A.device)
-    S = torch.empty((k, m), dtype=torch.float32, device=A.device)
-    lam = torch.empty((k,), dtype=torch.float64, device=A.device)
+    ctx = ctx or context(A.device if A.is_cuda else None)
+    S = _alloc((k, m), torch.float32, A)
+    lam = _alloc((k,), torch.float64, A)
     if omega is not None:
         _need(omega, torch.float64, "omega", 2)
     o = MfOpts(oversample, power_iters, int(bool(subspace)), _ptr(omega))

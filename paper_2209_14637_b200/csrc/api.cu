@@ -179,6 +179,72 @@ __global__ void unpad_gather_kernel(const double* __restrict__ pad, long long pe
   out[b] = pad[p * per + (b - (p * B) / P)];
 }
 
+// ------------------------------------------------------------------------------ whole-array staging
+// Host pointers for the entry points that consume whole arrays (two-sided, matrix-free): every host
+// buffer gets a device copy in a ctx staging slot (inputs copied in on the ctx stream, outputs copied
+// back), and the call returns after the stream is synchronised -- the synchronous host semantics of the
+// one-sided entry points (which additionally chunk A through pinned double buffers).  Device buffers are
+// used in place and must be 16-byte aligned (TMA rows).
+namespace {
+struct Stager {
+  tsk::Ctx* c;
+  int next = tsk::WS_STAGE_0;
+  tsk_status st = TSK_OK;
+  bool any = false;
+  struct Out {
+    void* dev;
+    void* user;
+    size_t bytes;
+  };
+  Out outs[8];
+  int nout = 0;
+  void* slot(size_t bytes) {
+    if (next > tsk::WS_STAGE_LAST) {
+      st = TSK_EINVAL;
+      return nullptr;
+    }
+    void* d = c->workspace(next++, bytes);
+    if (!d) st = TSK_ENOMEM;
+    any = true;
+    return d;
+  }
+  template <class T>
+  const T* in(const T* user, size_t bytes) {
+    if (!user || st != TSK_OK) return user;
+    if (is_device_ptr(user)) {
+      if (misaligned16(user)) st = TSK_ESHAPE;
+      return user;
+    }
+    void* d = slot(bytes);
+    if (d && cudaMemcpyAsync(d, user, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess) st = TSK_ECUDA;
+    return reinterpret_cast<const T*>(d);
+  }
+  template <class T>
+  T* out(T* user, size_t bytes) {
+    if (!user || st != TSK_OK) return user;
+    if (is_device_ptr(user)) {
+      if (misaligned16(user) && sizeof(T) == 4) st = TSK_ESHAPE;
+      return user;
+    }
+    void* d = slot(bytes);
+    if (d) outs[nout++] = Out{d, user, bytes};
+    return reinterpret_cast<T*>(d);
+  }
+  // copy the outputs back (also after a warning status) and synchronise when anything was staged
+  tsk_status finish(tsk_status s) {
+    if (is_error(s)) {
+      if (any) cudaStreamSynchronize(c->stream);
+      return s;
+    }
+    for (int i = 0; i < nout; ++i)
+      if (cudaMemcpyAsync(outs[i].user, outs[i].dev, outs[i].bytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+        return TSK_ECUDA;
+    if (any && cudaStreamSynchronize(c->stream) != cudaSuccess) return TSK_ECUDA;
+    return s;
+  }
+};
+}  // namespace
+
 extern "C" {
 
 tsk_status tsk_get_unique_id(unsigned char uid[128]) {
@@ -663,15 +729,19 @@ tsk_status scw_error(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const
 }
 
 // ------------------------------------------------------------------------------ two-sided variant
-// (device pointers only)
+// (host or device pointers)
 tsk_status sketch_gram_mode2(tsk_ctx ctx, const float* A, int64_t D, int m, int n, double* G64, int accumulate) {
   if (!ctx) return TSK_ENULL;
   if (!A || !G64) return TSK_ENULL;
   if (D < 1 || m < 1 || n < 1) return TSK_EINVAL;
   if ((m % 4) || (n % 4)) return TSK_ESHAPE;
-  if (!is_device_ptr(A) || !is_device_ptr(G64)) return TSK_EINVAL;
   cudaSetDevice(ctx->c.device);
-  return tsk::gram_mode2(&ctx->c, A, D, m, n, G64, accumulate);
+  Stager sg{&ctx->c};
+  const float* Ad = sg.in(A, (size_t)D * m * n * 4);
+  double* Gd = accumulate ? const_cast<double*>(sg.in(G64, (size_t)n * n * 8)) : sg.out(G64, (size_t)n * n * 8);
+  if (accumulate && Gd != G64 && sg.st == TSK_OK) sg.outs[sg.nout++] = Stager::Out{Gd, G64, (size_t)n * n * 8};
+  if (sg.st != TSK_OK) return sg.finish(sg.st);
+  return sg.finish(tsk::gram_mode2(&ctx->c, Ad, D, m, n, Gd, accumulate));
 }
 
 tsk_status sketch_train_two_sided(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, int l, float* S,
@@ -681,24 +751,37 @@ tsk_status sketch_train_two_sided(tsk_ctx ctx, const float* A, int64_t D, int m,
   if (D < 1 || m < 1 || n < 1 || k < 1 || k > m || l < 1 || l > n) return TSK_EINVAL;
   if ((m % 4) || (n % 4)) return TSK_ESHAPE;
   if ((m > 256 && k + 16 > 256) || (n > 256 && l + 16 > 256)) return TSK_EINVAL;
-  if (!is_device_ptr(A) || !is_device_ptr(S) || !is_device_ptr(W)) return TSK_EINVAL;
   cudaSetDevice(ctx->c.device);
-  return tsk::hooi_tucker2(&ctx->c, A, D, m, n, k, l, S, W, opts, info);
+  Stager sg{&ctx->c};
+  const float* Ad = sg.in(A, (size_t)D * m * n * 4);
+  float* Sd = sg.out(S, (size_t)k * m * 4);
+  float* Wd = sg.out(W, (size_t)l * n * 4);
+  if (sg.st != TSK_OK) return sg.finish(sg.st);
+  return sg.finish(tsk::hooi_tucker2(&ctx->c, Ad, D, m, n, k, l, Sd, Wd, opts, info));
 }
 
 // ------------------------------------------------------------------------------ matrix-free sketch
-// (device pointers only)
+// (host or device pointers)
 tsk_status sketch_train_matrix_free(tsk_ctx ctx, const float* A, int64_t D, int m, int n, int k, float* S,
                                     double* lambda, const tsk_mf_opts* opts, tsk_mf_info* info) {
   if (!ctx) return TSK_ENULL;
   if (!A || !S) return TSK_ENULL;
   if (D < 1 || m < 1 || n < 1 || k < 1 || k > m) return TSK_EINVAL;
   if (n % 4) return TSK_ESHAPE;
-  if (!is_device_ptr(A) || !is_device_ptr(S) || (lambda && !is_device_ptr(lambda)) ||
-      (opts && opts->omega && !is_device_ptr(opts->omega)))
-    return TSK_EINVAL;
   cudaSetDevice(ctx->c.device);
-  return tsk::matrix_free_sketch(&ctx->c, A, D, m, n, k, S, lambda, opts, info);
+  Stager sg{&ctx->c};
+  const float* Ad = sg.in(A, (size_t)D * m * n * 4);
+  float* Sd = sg.out(S, (size_t)k * m * 4);
+  double* ld = sg.out(lambda, (size_t)k * 8);
+  tsk_mf_opts o{};
+  if (opts) o = *opts;
+  if (o.omega) {  // the start block [m][p], p as matrix_free_sketch derives it
+    int pp = k + (o.oversample > 0 ? o.oversample : 16);
+    pp = std::min((pp + 3) & ~3, m);
+    o.omega = sg.in(o.omega, (size_t)m * pp * 8);
+  }
+  if (sg.st != TSK_OK) return sg.finish(sg.st);
+  return sg.finish(tsk::matrix_free_sketch(&ctx->c, Ad, D, m, n, k, Sd, ld, opts ? &o : nullptr, info));
 }
 
 static tsk_status scw2_common(tsk_ctx ctx, const float* A, int64_t B, int m, int n, const float* S, int k,
@@ -715,11 +798,17 @@ static tsk_status scw2_common(tsk_ctx ctx, const float* A, int64_t B, int m, int
   }
   if (r > std::min(m, n) || r > 64) return TSK_EINVAL;
   if (B == 0) return warn;
-  if (!is_device_ptr(A) || !is_device_ptr(S) || !is_device_ptr(W) || (L && !is_device_ptr(L)) ||
-      (R && !is_device_ptr(R)) || (sigma && !is_device_ptr(sigma)) || (err && !is_device_ptr(err)))
-    return TSK_EINVAL;
   cudaSetDevice(ctx->c.device);
-  tsk_status s = tsk::scw2_run(&ctx->c, A, B, m, n, S, k, W, l, r, L, R, sigma, err);
+  Stager sg{&ctx->c};
+  const float* Ad = sg.in(A, (size_t)B * m * n * 4);
+  const float* Sd = sg.in(S, (size_t)k * m * 4);
+  const float* Wd = sg.in(W, (size_t)l * n * 4);
+  float* Ld = sg.out(L, (size_t)B * m * r * 4);
+  float* Rd = sg.out(R, (size_t)B * n * r * 4);
+  float* sd = sg.out(sigma, (size_t)B * r * 4);
+  double* ed = sg.out(err, (size_t)B * 8);
+  if (sg.st != TSK_OK) return sg.finish(sg.st);
+  tsk_status s = sg.finish(tsk::scw2_run(&ctx->c, Ad, B, m, n, Sd, k, Wd, l, r, Ld, Rd, sd, ed));
   return is_error(s) ? s : warn;
 }
 

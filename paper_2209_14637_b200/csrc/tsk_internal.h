@@ -70,6 +70,8 @@ enum WorkspaceId {
   WS_SYEV,         // small symmetric eigensolver: reflectors, tridiagonal, scratch
   WS_GATHER,       // tsk_allgather_errors: padded [P][per] gather buffer
   WS_SCW_EIG,    // per-part eigensolver scratch of the batched SCW (its parts run concurrently)
+  WS_STAGE_0,    // host-pointer staging of the whole-array entry points (two-sided, matrix-free): 8 slots
+  WS_STAGE_LAST = WS_STAGE_0 + 7,
   WS_COUNT
 };
 

@@ -123,7 +123,8 @@ def test_matrix_free_rejects_bad_arguments():
     with pytest.raises(tsk.TskError):
         tsk.sketch_train_matrix_free(A[:, :, :46].contiguous(), 4)            # n % 4
     with pytest.raises(tsk.TskError):
-        tsk.sketch_train_matrix_free(A.cpu(), 4)                              # host memory
+        tsk.sketch_train_matrix_free(A[:, :, 1:45].contiguous()[:, :, :44].contiguous().view(-1)[1:1 + 2 * 64 * 40]
+                                     .view(2, 64, 40), 4)                     # device A not 16-B aligned
 
 
 def test_matrix_free_c4_scale():

@@ -443,3 +443,33 @@ def test_pinned_host_input_is_synchronous():
     tsk.sketch_gram(A[20:].cuda(), G64=G_ref, accumulate=True)
     torch.cuda.synchronize()
     assert torch.equal(G, G_ref)
+
+
+def test_host_pointers_two_sided_and_matrix_free():
+    """The whole-array entry points (two-sided, matrix-free) accept host arrays (staged, synchronous) and
+    give bit-identical results to the device call on the same data (include/tsketch.h staging contract)."""
+    c = datagen.CONFIGS["C1"]
+    A = datagen.generate(c, "train")
+    T = datagen.generate(c, "test", 0, 8)
+    Ad, Td = A.cuda(), T.cuda()
+    G_h = tsk.sketch_gram_mode2(A)
+    G_d = tsk.sketch_gram_mode2(Ad)
+    assert not G_h.is_cuda
+    np.testing.assert_array_equal(G_h.numpy(), G_d.cpu().numpy())
+    S_h, W_h, info_h, st_h = tsk.sketch_train_two_sided(A, 10, 8, max_sweeps=2)
+    S_d, W_d, info_d, st_d = tsk.sketch_train_two_sided(Ad, 10, 8, max_sweeps=2)
+    assert st_h == st_d and not S_h.is_cuda
+    np.testing.assert_array_equal(S_h.numpy(), S_d.cpu().numpy())
+    np.testing.assert_array_equal(W_h.numpy(), W_d.cpu().numpy())
+    e_h = tsk.two_sided_scw_error(T, S_h, W_h, 5)
+    e_d = tsk.two_sided_scw_error(Td, S_d, W_d, 5)
+    assert not e_h.is_cuda
+    np.testing.assert_array_equal(e_h.numpy(), e_d.cpu().numpy())
+    L_h, R_h, s_h = tsk.sketch_apply_two_sided_scw(T, S_h, W_h, 5)
+    L_d, R_d, s_d = tsk.sketch_apply_two_sided_scw(Td, S_d, W_d, 5)
+    np.testing.assert_array_equal(L_h.numpy(), L_d.cpu().numpy())
+    np.testing.assert_array_equal(s_h.numpy(), s_d.cpu().numpy())
+    Sm_h, lam_h, _, _ = tsk.sketch_train_matrix_free(A, 6)
+    Sm_d, lam_d, _, _ = tsk.sketch_train_matrix_free(Ad, 6)
+    np.testing.assert_array_equal(Sm_h.numpy(), Sm_d.cpu().numpy())
+    np.testing.assert_array_equal(lam_h.numpy(), lam_d.cpu().numpy())
