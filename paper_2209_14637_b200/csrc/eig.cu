@@ -356,132 +356,6 @@ static cudaError_t launch_gq(int mt, int splits, cudaStream_t s, const double* G
   return cudaLaunchKernelEx(&cfg, gq_f64_kernel<JN>, G, m, m, Y, Yp, q, ldy, alpha, beta, gamma, Out, splits);
 }
 
-// DMMA version of gq_f64_kernel (used for every q): the CTA's whole split of K streams through a
-// 4-stage cp.async ring of 32-deep chunks (G tile 64 x 32, Y tile 32 x BN); 8 warps as 2 (rows) x 4
-// (columns), warp tile 32 x 8 NT of m8n8k4 fp64 MMAs: per 4-deep step 4 + NT fragment loads feed 4 NT
-// MMAs (the DFMA kernel above loaded 10 operands per 24 FMAs per thread and ran at ~20 % of the fp64
-// rate).  Padded strides (36, BN + 4 doubles) make every fragment load conflict-free.  The split-K
-// partial tiles are reduced over the cluster's DSMEM as before (fixed order: deterministic).
-constexpr int kDmKC = 32, kDmStages = 4, kDmLDA = kDmKC + 4;
-template <int NT>
-constexpr size_t gq_dmma_smem() {
-  return (size_t)kDmStages * (64 * kDmLDA + kDmKC * (32 * NT + 4)) * sizeof(double);
-}
-template <int NT>
-__global__ void __launch_bounds__(256) gq_dmma_kernel(const double* __restrict__ G, int m, int ldg,
-                                                      const double* __restrict__ Y, const double* __restrict__ Yp,
-                                                      int q, int ldy, double alpha, double beta, double gamma,
-                                                      double* __restrict__ Out, int splits) {
-  constexpr int BN = 32 * NT, LDB = BN + 4;
-  constexpr int ASZ = 64 * kDmLDA, STG = ASZ + kDmKC * LDB;
-  extern __shared__ double dm_sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int i0 = blockIdx.x * 64, sp = blockIdx.y;
-  const int k0 = (int)((long long)sp * m / splits), k1 = (int)((long long)(sp + 1) * m / splits);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, wm = warp >> 2, wn = warp & 3;
-  const int nch = (k1 - k0 + kDmKC - 1) / kDmKC;
-  auto issue = [&](int c) {
-    double* As = dm_sm + (c % kDmStages) * STG;
-    double* Bs = As + ASZ;
-    const int kb = k0 + c * kDmKC;
-#pragma unroll
-    for (int u = 0; u < 64 * kDmKC / 256; ++u) {
-      const int e = tid + 256 * u, r = e / kDmKC, kc = e % kDmKC;
-      const int row = i0 + r, col = kb + kc;
-      const bool ok = row < m && col < k1;
-      cp_async8(As + r * kDmLDA + kc, ok ? G + (size_t)row * ldg + col : G, ok ? 8 : 0);
-    }
-#pragma unroll
-    for (int u = 0; u < kDmKC * BN / 256; ++u) {
-      const int e = tid + 256 * u, kc = e / BN, c2 = e % BN;
-      const int kr = kb + kc;
-      const bool ok = kr < k1 && c2 < q;
-      cp_async8(Bs + kc * LDB + c2, ok ? Y + (size_t)kr * ldy + c2 : Y, ok ? 8 : 0);
-    }
-  };
-  double acc[4][NT][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll
-  for (int c = 0; c < kDmStages - 1; ++c) {
-    if (c < nch) issue(c);
-    cp_async_commit();
-  }
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait<kDmStages - 2>();
-    __syncthreads();  // chunk c landed for every thread; chunk c - 1's slot is free
-    if (c + kDmStages - 1 < nch) issue(c + kDmStages - 1);
-    cp_async_commit();
-    const double* As = dm_sm + (c % kDmStages) * STG + (wm * 32 + (lane >> 2)) * kDmLDA + (lane & 3);
-    const double* Bs = dm_sm + (c % kDmStages) * STG + ASZ + (lane & 3) * LDB + wn * 8 * NT + (lane >> 2);
-#pragma unroll
-    for (int k4 = 0; k4 < kDmKC / 4; ++k4) {
-      double a[4], b[NT];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[8 * i * kDmLDA + 4 * k4];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = Bs[4 * k4 * LDB + 8 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma_m8n8k4(acc[i][j], a[i], b[j]);
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  double* Ps = dm_sm;  // [64][BN] partial tile (the ring is free)
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int r = wm * 32 + 8 * i + (lane >> 2), c2 = wn * 8 * NT + 8 * j + 2 * (lane & 3);
-      Ps[r * BN + c2] = acc[i][j][0];
-      Ps[r * BN + c2 + 1] = acc[i][j][1];
-    }
-  cluster.sync();
-  for (int e = tid; e < 64 * BN; e += 256) {
-    const int r = e / BN, c2 = e % BN;
-    if (r % splits != sp) continue;
-    const int row = i0 + r;
-    if (row >= m || c2 >= q) continue;
-    double sacc = 0.0;
-    for (int t = 0; t < splits; ++t) sacc += cluster.map_shared_rank(Ps, t)[e];
-    double v = alpha * sacc;
-    if (beta != 0.0) v = fma(beta, Y[(size_t)row * ldy + c2], v);
-    if (gamma != 0.0) v = fma(gamma, Yp[(size_t)row * ldy + c2], v);
-    Out[(size_t)row * ldy + c2] = v;
-  }
-  cluster.sync();
-}
-
-template <int NT>
-static cudaError_t launch_gq_dmma(int mt, int splits, cudaStream_t s, const double* G, int m, const double* Y,
-                                  const double* Yp, int q, int ldy, double alpha, double beta, double gamma,
-                                  double* Out) {
-  constexpr size_t smem = gq_dmma_smem<NT>();
-  static uint64_t attr = 0;
-  if (!(attr & device_bit())) {
-    cudaFuncSetAttribute(gq_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(gq_dmma_kernel<NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr |= device_bit();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(mt, splits, 1);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = splits;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gq_dmma_kernel<NT>, G, m, m, Y, Yp, q, ldy, alpha, beta, gamma, Out, splits);
-}
-
 // Out = alpha G Y + beta Y + gamma Yp for Y [m][ldy] with q <= 128 columns (fp64)
 static tsk_status gq_f64(Ctx* ctx, const double* G, int m, const double* Y, const double* Yp, int q, int ldy,
                          double alpha, double beta, double gamma, double* Out) {
@@ -492,14 +366,6 @@ static tsk_status gq_f64(Ctx* ctx, const double* G, int m, const double* Y, cons
   const int splits = std::max(1, std::min(std::min((ctx->num_sms + mt - 1) / mt, std::max(1, m / 64)), 8));
   cudaStream_t s = ctx->stream;
   cudaError_t e;
-  if (getenv("TSK_GQ_DMMA")) {
-    switch ((q + 31) / 32) {
-      case 1: e = launch_gq_dmma<1>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 2: e = launch_gq_dmma<2>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 3: e = launch_gq_dmma<3>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      default: e = launch_gq_dmma<4>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    }
-  } else
   switch (JN) {
     case 1: e = launch_gq<1>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
     case 2: e = launch_gq<2>(mt, splits, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;

@@ -84,26 +84,6 @@ TSK_DEV uint32_t tf32_rn(float x) {
   return r;
 }
 
-// ---------------------------------------------------------------- Ampere-style async copies + fp64 MMA
-// 8-byte cp.async global -> shared; src_bytes 0 zero-fills the destination (out-of-range element)
-TSK_DEV void cp_async8(void* smem_dst, const void* gsrc, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(src_bytes)
-               : "memory");
-}
-TSK_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-TSK_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// D = A B + D, fp64 m8n8k4 (row.col): lane holds A[lane/4][lane%4], B[k = lane%4][n = lane/4],
-// D[lane/4][2 (lane%4) + {0, 1}].  37 TF/s on one B200 (scripts/dmma_bench.cu), vs 34 for DFMA, with
-// a quarter of DFMA's operand traffic per flop.
-TSK_DEV void dmma_m8n8k4(double (&d)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
-}
-
 // ---------------------------------------------------------------- L2 cache-policy hinted accesses
 TSK_DEV uint64_t l2_policy_evict_last() {
   uint64_t p;
