@@ -70,13 +70,18 @@ struct GemmArgs {
   long long dstride;
   int ldd;
   const int* only;   // batch mode: problems b with only[b] == 0 are skipped by every role (null: all)
-  double* sq_part;   // TS kernel: [U][4] fp64 sums of the squared X elements of each unit (transform warps)
+  double* sq_part;   // TS kernel: [U][8] fp64 sums of the squared X elements of each unit (transform warps)
 };
 
 // batch mode with a problem mask: unit u belongs to a skipped problem (same test in every role, so the
-// ring / accumulator phases stay in step)
-__device__ __forceinline__ bool unit_skipped(const GemmArgs& a, int u) {
-  return a.only != nullptr && a.only[(u % a.T) / a.T0] == 0;
+// ring / accumulator phases stay in step).  The mask is copied to shared memory in the prologue when the
+// batch has <= kOnlyMax problems (a CTA walks ~U / 148 units; one dependent global load per unit cost
+// ~65 us on a launch whose units were all skipped).
+constexpr int kOnlyMax = 256;  // 1 KB: the kYT variant has 225 KB of dynamic shared memory
+__device__ __forceinline__ bool unit_skipped(const GemmArgs& a, const int* s_only, int u) {
+  if (a.only == nullptr) return false;
+  const int b = (u % a.T) / a.T0;
+  return (s_only ? s_only[b] : a.only[b]) == 0;
 }
 
 __device__ __forceinline__ void tile_coords(const GemmArgs& a, int t, int& bi, int& bj) {
@@ -388,7 +393,21 @@ constexpr int kTsLoStages = 3;
 // toward zero (~3e-7 relative on SCW's AV, which the Pythagorean error reads at first order, reading
 // c17).  Y keeps the hardware-truncated raw tile as hi; its lo part is rounded to nearest.
 constexpr bool kYLoRn = true;
-constexpr int kTsSmemBytes = (kRawStages * 2 + kTsLoStages) * kTileBytes + 1024 + 256;
+// Ring geometry: [X | Y] raw stages and [L_Y] (or, kYT, [H_Y | L_Y]) lo stages.  With N = 64 the Y tiles
+// are half size, so the raw ring packs 7 stages of 24 KB instead of 5 of 32 KB: the SCW products (SA, AV)
+// stream A from HBM and are latency-bound on the bytes in flight per SM.
+template <bool kN64, bool kYT>
+constexpr int ts_raw_stages() { return kYT ? kRawStages - 1 : (kN64 ? 7 : kRawStages); }
+template <bool kN64, bool kYT>
+constexpr int ts_raw_stage_bytes() { return kYT ? 2 * kTileBytes : kTileBytes + (kN64 ? kTileBytes / 2 : kTileBytes); }
+template <bool kN64, bool kYT>
+constexpr int ts_lo_stage_bytes() { return kYT ? 2 * kTileBytes : (kN64 ? kTileBytes / 2 : kTileBytes); }
+template <bool kN64, bool kYT>
+constexpr int ts_smem_bytes() {
+  return ts_raw_stages<kN64, kYT>() * ts_raw_stage_bytes<kN64, kYT>() + kTsLoStages * ts_lo_stage_bytes<kN64, kYT>() +
+         1024 + 256;
+}
+constexpr int kTsSmemBytes = ts_smem_bytes<false, false>();
 constexpr uint32_t kTsAccCols = 128;
 constexpr uint32_t kTsAStageCols = 64;
 
@@ -398,12 +417,17 @@ template <bool kN64, bool kYT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                           const GemmArgs a) {
-  constexpr int RS = kYT ? kRawStages - 1 : kRawStages;   // raw ring depth
-  constexpr int LB = kYT ? 2 * kTileBytes : kTileBytes;   // lo stage: [L_Y] or [H_Y | L_Y]
+  constexpr int RS = ts_raw_stages<kN64, kYT>();          // raw ring depth
+  constexpr int RSB = ts_raw_stage_bytes<kN64, kYT>();    // raw stage: [X | Y] (Y = bn x 32 fp32)
+  constexpr int LB = ts_lo_stage_bytes<kN64, kYT>();      // lo stage: [L_Y] or [H_Y | L_Y]
+  // N = 64 (SCW's SA / AV products): the split transform is the critical path (one warp per SM
+  // sub-partition, latency-bound), so warps 12-15 join it -- two warps per TMEM lane quadrant, each
+  // converting 16 of the chunk's 32 K-columns -- and the 64-column epilogue runs on warps 8-11
+  constexpr bool kSplitT = kN64 && !kYT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* raw_base = smem;                                 // [RS][X|Y]
-  uint8_t* lo_base = smem + RS * 2 * kTileBytes;            // [kTsLoStages][LB]
+  uint8_t* lo_base = smem + RS * RSB;                       // [kTsLoStages][LB]
   uint64_t* bars = reinterpret_cast<uint64_t*>(lo_base + kTsLoStages * LB);
   uint64_t* rfull = bars;
   uint64_t* rempty = rfull + RS;
@@ -424,14 +448,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&rempty[i], 1);
     }
     for (int i = 0; i < kTsLoStages; ++i) {
-      mbar_init(&lfull[i], 4);
+      mbar_init(&lfull[i], kSplitT ? 8 : 4);
       mbar_init(&lempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&accf[i], 1);
-      mbar_init(&acce[i], 8);
+      mbar_init(&acce[i], kSplitT ? 4 : 8);
     }
     fence_barrier_init();
+  }
+  __shared__ int s_only_buf[kOnlyMax];
+  const int* s_only = nullptr;
+  if (a.only && a.T / a.T0 <= kOnlyMax) {
+    for (int i = threadIdx.x; i < a.T / a.T0; i += blockDim.x) s_only_buf[i] = a.only[i];
+    s_only = s_only_buf;
   }
   if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -439,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto raw_ptr = [&](int st, int which) { return raw_base + (st * 2 + which) * kTileBytes; };
+  auto raw_ptr = [&](int st, int which) { return raw_base + st * RSB + which * kTileBytes; };
   auto lo_ptr = [&](int st) { return lo_base + st * LB; };
 
   if (warp == 0) {
@@ -455,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ybytes = (uint32_t)(a.bn * kBK * 4);
       long long idx = 0;  // CTA-wide chunk index (stage = idx % RS, use = idx / RS)
       for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-        if (unit_skipped(a, u)) continue;
+        if (unit_skipped(a, s_only, u)) continue;
         int t, bi, bj;
         long long q0, q1;
         unit_range(a, u, t, q0, q1);
@@ -512,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int ab = 0;
       uint32_t aph = 0;
       for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-        if (unit_skipped(a, u)) continue;
+        if (unit_skipped(a, s_only, u)) continue;
         int t, bi, bj;
         long long q0, q1;
         unit_range(a, u, t, q0, q1);
@@ -555,14 +585,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if ((warp >= 4 && warp < 8) || (kSplitT && warp >= 12)) {
     // ===================== transform: X rows -> TMEM (H, L); Y tile -> L_Y in shared memory ========
-    const int tt = threadIdx.x - 128;  // 0..127 = tile row handled for the TMEM A operand
-    const int quad = warp & 3;         // == tt / 32: the TMEM lane quadrant of this warp
+    const int quad = warp & 3;         // the TMEM lane quadrant of this warp
+    const int tt = quad * 32 + lane;   // 0..127 = tile row handled for the TMEM A operand
+    constexpr int NC = kSplitT ? 16 : 32;  // K-columns of the chunk converted by this warp
+    const int grp = (kSplitT && warp >= 12) ? 1 : 0;
+    const int c0 = grp * NC;
     int rs = 0, ls = 0;
     uint32_t rph = 0, lph = 0;
     for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-      if (unit_skipped(a, u)) continue;
+      if (unit_skipped(a, s_only, u)) continue;
       int t, bi, bj;
       long long q0, q1;
       unit_range(a, u, t, q0, q1);
@@ -576,27 +609,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (1) row tt of X (128-B swizzled row: 16-B chunk c at position c ^ (tt & 7)); for a
         // transposed X the raw tile is [32 K][128 M] unswizzled and row tt of X is column tt
         {
-          uint32_t hi[32], lo[32];
+          uint32_t hi[NC], lo[NC];
           if (a.xt) {
             const float* xcol = reinterpret_cast<const float*>(raw_ptr(rs, 0)) + tt;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const float e = xcol[c * kBM];
+            for (int c = 0; c < NC; ++c) {
+              const float e = xcol[(c0 + c) * kBM];
               const uint32_t h = tf32_rn(e);
               hi[c] = h;
               lo[c] = __float_as_uint(e - __uint_as_float(h));
             }
-            if (a.sq_part) {  // fp32 within the chunk (32 positive terms), fp64 across chunks
+            if (a.sq_part) {  // fp32 within the chunk (<= 32 positive terms), fp64 across chunks
               float cs = 0.f;
 #pragma unroll
-              for (int c = 0; c < 32; ++c) cs = fmaf(xcol[c * kBM], xcol[c * kBM], cs);
+              for (int c = 0; c < NC; ++c) cs = fmaf(xcol[(c0 + c) * kBM], xcol[(c0 + c) * kBM], cs);
               sq += (double)cs;
             }
           } else {
             const uint32_t xrow = smem_u32(raw_ptr(rs, 0)) + (uint32_t)tt * 128u;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float4 v = lds_f4(xrow + (uint32_t)((c ^ (tt & 7)) * 16));
+            for (int c = 0; c < NC / 4; ++c) {
+              const float4 v = lds_f4(xrow + (uint32_t)(((c0 / 4 + c) ^ (tt & 7)) * 16));
               const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -613,8 +646,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           const uint32_t ta = tmem_base + ((uint32_t)(quad * 32) << 16) + 2 * kTsAccCols + (uint32_t)ls * kTsAStageCols;
-          tmem_st_32x32b_x32(ta, hi);
-          tmem_st_32x32b_x32(ta + 32, lo);
+          if constexpr (NC == 32) {
+            tmem_st_32x32b_x32(ta, hi);
+            tmem_st_32x32b_x32(ta + 32, lo);
+          } else {
+            tmem_st_32x32b_x16(ta + c0, hi);
+            tmem_st_32x32b_x16(ta + 32 + c0, lo);
+          }
         }
         // (2) the B-side lo part: L_Y (or L_X for a diagonal tile) in the swizzled smem layout; for
         // a transposed Y, row tt of Y is column tt of the raw [32 K][bn N] tile and both H_Y and
@@ -645,8 +683,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t src = smem_u32(raw_ptr(rs, diag ? 0 : 1));
           const uint32_t dst = smem_u32(lo_ptr(ls));
           const int nyv = a.bn * (kBK * 4 / 16);  // float4 of the bn used rows
-          for (int i = 0; i < nyv / 128; ++i) {
-            const uint32_t off = (uint32_t)(i * 128 + tt) * 16u;
+          constexpr int kTT = kSplitT ? 256 : 128;  // transform threads
+          for (int i = grp * 128 + tt; i < nyv; i += kTT) {
+            const uint32_t off = (uint32_t)i * 16u;
             const float4 v = lds_f4(src + off);
             float4 l;
             if (kYLoRn) {
@@ -671,26 +710,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (++rs == RS) { rs = 0; rph ^= 1; }
         if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
       }
-      if (a.sq_part) {  // fixed-order warp reduction: one partial per (unit, transform warp)
+      if (a.sq_part) {  // fixed-order warp reduction: one partial per (unit, transform warp), 8 per unit
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) a.sq_part[(size_t)u * 4 + quad] = sq;
+        if (lane == 0) {
+          a.sq_part[(size_t)u * 8 + grp * 4 + quad] = sq;
+          if (!kSplitT) a.sq_part[(size_t)u * 8 + 4 + quad] = 0.0;
+        }
       }
     }
   } else if (warp >= 8) {
     // ===================== epilogue: TMEM chains -> fp32 registers -> fp64 partials =====================
     const int e = warp - 8;
     const int quad = warp & 3;
-    // columns per epilogue warp: 64 of the 128-wide accumulator, or 32 of a 64-wide output (N = 64:
-    // both warp groups drain, and a thread holds 32 + 2 x 32 values instead of 64 + 2 x 32 -- no spills)
-    constexpr int kEC = kN64 ? 32 : 64;
-    const int col0 = (e >> 2) * kEC;
+    // columns per epilogue warp: 64 of the 128-wide accumulator; for N = 64 all 64 (kSplitT: warps
+    // 8-11 only, drained 16 columns at a time) or 32 (kYT: both warp groups drain) -- no spills
+    constexpr int kEC = kN64 ? (kSplitT ? 64 : 32) : 64;
+    const int col0 = kSplitT ? 0 : (e >> 2) * kEC;
     const int row = quad * 32 + lane;
     int ab = 0;
     uint32_t aph = 0;
     const bool has_cols = col0 < a.bn;
     for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
-      if (unit_skipped(a, u)) continue;
+      if (unit_skipped(a, s_only, u)) continue;
       int t;
       long long q0, q1;
       unit_range(a, u, t, q0, q1);
@@ -768,7 +810,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)ab * kTsAccCols + col0;
         if (has_cols) {
-          if constexpr (kN64) {  // separate accumulators: columns [0,64) = H H^T, [64,128) = cross terms
+          if constexpr (kSplitT) {  // separate accumulators: columns [0,64) = H H^T, [64,128) = cross terms
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              uint32_t r[16], x[16];
+              tmem_ld_32x32b_x16(taddr + h * 16, r);
+              tmem_ld_32x32b_x16(taddr + 64 + h * 16, x);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) sum[h * 16 + i] += __uint_as_float(r[i]) + __uint_as_float(x[i]);
+            }
+          } else if constexpr (kN64) {
             uint32_t r[32], x[32];
             tmem_ld_32x32b_x32(taddr, r);
             tmem_ld_32x32b_x32(taddr + 64, x);
@@ -1063,7 +1115,9 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.progress = prog;
   if (cudaMemsetAsync(prog, 0, (size_t)a.U * sizeof(unsigned), ctx->stream) != cudaSuccess) return TSK_ECUDA;
 
-  constexpr int kTsYtSmemBytes = ((kRawStages - 1) * 2 + 2 * kTsLoStages) * kTileBytes + 1024 + 256;
+  constexpr int kTsYtSmemBytes = ts_smem_bytes<false, true>();
+  constexpr int kTs64SmemBytes = ts_smem_bytes<true, false>();
+  static_assert(ts_smem_bytes<true, true>() == kTsYtSmemBytes, "kYT geometry does not depend on N");
   static uint64_t attr_set = 0;
   if (!(attr_set & device_bit())) {
     if (cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
@@ -1071,7 +1125,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
         cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kTsSmemBytes) != cudaSuccess ||
         cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kTsSmemBytes) != cudaSuccess ||
+                             kTs64SmemBytes) != cudaSuccess ||
         cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kTsYtSmemBytes) != cudaSuccess ||
         cudaFuncSetAttribute(gemm_tf32x3_ts_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1088,7 +1142,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
       else
         gemm_tf32x3_ts_kernel<false, true><<<grid, kThreads, kTsYtSmemBytes, ctx->stream>>>(mx, my, a);
     } else if (a.bn == 64) {
-      gemm_tf32x3_ts_kernel<true, false><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
+      gemm_tf32x3_ts_kernel<true, false><<<grid, kThreads, kTs64SmemBytes, ctx->stream>>>(mx, my, a);
     } else {
       gemm_tf32x3_ts_kernel<false, false><<<grid, kThreads, kTsSmemBytes, ctx->stream>>>(mx, my, a);
     }

@@ -519,9 +519,9 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   // factor row pitch: r for the caller's L / R, r rounded up to 4 (16-byte TMA rows) for the error path
   const int ldf = (L || R) ? r : (r + 3) & ~3;
   float* Lw = reinterpret_cast<float*>(ctx->workspace(WS_SCW_4, chunk * ((size_t)m + n) * ldf * 4));
-  // residual partials, then the ||A||^2 partials of the SA product (4 per unit, nb(n, 128) units per
+  // residual partials, then the ||A||^2 partials of the SA product (8 per unit, nb(n, 128) units per
   // matrix) and the dense-residual marks of the Pythagorean error path
-  const int sq_per = (int)nb(n, 128) * 4;
+  const int sq_per = (int)nb(n, 128) * 8;
   double* part = reinterpret_cast<double*>(
       ctx->workspace(WS_SCW_5, chunk * ((size_t)tiles + sq_per) * 8 + chunk * 4 + 64));
   if (!Bm_all || !Vt_all || !Zt_all || !small || !Lw || !part) return TSK_ENOMEM;

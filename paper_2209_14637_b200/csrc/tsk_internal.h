@@ -195,7 +195,7 @@ struct GemmProblem {
   double* res_part = nullptr;
   // batch mode: only problems b with only[b] != 0 are computed (the others' outputs are not written)
   const int* only = nullptr;
-  // TS kernel, batch mode: sq_part[unit][4] = fp64 sums of the squared X elements each unit reads
+  // TS kernel, batch mode: sq_part[unit][8] = fp64 sums of the squared X elements each unit reads
   // (unit u of problem b: u = b * tiles + tile; every X element of a problem in exactly one unit when N
   // fits one column block)
   double* sq_part = nullptr;
