@@ -248,6 +248,37 @@ def test_scw_exactly_low_rank_is_exact():
     assert np.all(err <= 1e-6 * fro)
 
 
+@pytest.mark.parametrize("eta", [1e-3, 3e-2])
+def test_scw_error_fallback_mixed_batch(eta):
+    """scw_error's Pythagorean error (reading c17) and its dense-residual fallback in ONE launch: a batch
+    mixing near-low-rank matrices (rank 5 + noise eta: err^2 / ||A||^2 ~ eta^2, below the 3e-3 threshold
+    for eta = 1e-3 -> dense residual) with ordinary ones (Pythagorean), interleaved, against the oracle's
+    Algorithm 1 errors with the same S (per-matrix BASELINE tolerance), and against mode 1 (dense for
+    all) within the same tolerance."""
+    base = datagen.CONFIGS["C1"]
+    near = datagen.lowrank("C1", rank=5).replace(eta=eta)
+    A = datagen.generate(near, "train")  # S captures the near-low-rank stream's subspace
+    S, _, _, _ = tsk.sketch_train(A.cuda(), base.k)
+    T = torch.empty((2 * base.D_test, base.m, base.n), dtype=torch.float32)
+    T[0::2] = datagen.generate(base, "test")
+    T[1::2] = datagen.generate(near, "test")
+    e = tsk.scw_error(T.cuda(), S, base.r).cpu().numpy()
+    Tn = T.numpy()
+    e_o = oscw.scw_errors(Tn, S.cpu().double().numpy(), base.r)
+    fro = np.linalg.norm(Tn.reshape(Tn.shape[0], -1).astype(np.float64), axis=1)
+    assert np.all(np.abs(e - e_o) <= 1e-4 * e_o + 1e-6 * fro), np.max(np.abs(e - e_o) / e_o)
+    try:
+        tsk.set_scw_error_mode(1)
+        e_d = tsk.scw_error(T.cuda(), S, base.r).cpu().numpy()
+    finally:
+        tsk.set_scw_error_mode(0)
+    assert np.all(np.abs(e - e_d) <= 1e-4 * e_d + 1e-6 * fro)
+    ratio = (e_o / fro) ** 2
+    if eta < 1e-2:  # the near-low-rank half is under the threshold: those entries ARE the dense residual
+        assert np.all(ratio[1::2] < 3e-3)
+        np.testing.assert_array_equal(e[1::2], e_d[1::2])
+
+
 def test_scw_square_sketch_is_eckart_young():
     """k = m: S orthogonal, SCW = [A]_r."""
     rng = np.random.default_rng(3)
