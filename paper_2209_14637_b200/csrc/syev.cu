@@ -28,7 +28,35 @@
 namespace tsk {
 
 constexpr int kTrdThreads = 512;
+#ifdef TSK_TRD_PROF
+__device__ long long trd_prof[4];  // diagnostic build only: cycles of the three phases of trd_kernel's steps
+#endif
 constexpr int kTrdSmemMaxP = 160;  // A (p x (p+1) fp64) in shared memory up to p = 160
+
+// fp64 reciprocal / square root without IEEE rounding: the MUFU seed (~2^-22) and two Newton steps
+// (quadratic: beyond 2^-53), a dependent chain of ~6 FMAs instead of the correctly rounded library
+// sequences (__drcp_rn, sqrt: ~150-300 cycles each with their special-case branches) -- the Householder
+// step of trd_kernel evaluates one square root and two reciprocals on its critical path.  Finite positive
+// (rcp: nonzero) arguments only.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * r, r, 0.5);
+  r = fma(r, e, r);
+  e = fma(-h * r, r, 0.5);
+  r = fma(r, e, r);
+  const double s0 = x * r;                 // sqrt(x) to ~1 ulp; one more correction step
+  return fma(fma(-s0, s0, x), 0.5 * r, s0);
+}
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -45,7 +73,11 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // the product A v_j -- one pass over A and three barriers per step.  Thread (ty, tx) of the 16 x 32
 // layout owns rows ty + 16 r and columns tx + 32 c of the trailing block; row sums are reduced
 // across the warp.  KR x KC bounds the rows / columns per thread (8 x 4 for p <= 129).
-template <bool kSmem, int KR, int KC>
+// kRow (p <= 129, A in shared memory; used up to p = 88): the fused pass is row-parallel instead -- four threads per row,
+// each a strided quarter of the columns, reduced with two shuffles (the 16 x 32 layout's butterfly over
+// 32 lanes and its 8 x 4 register tile made that pass a ~1400-cycle latency floor per step: measured with
+// -DTSK_TRD_PROF, phase 2 of a p = 76 step took 1950 cycles of 4350).
+template <bool kSmem, int KR, int KC, bool kRow = false>
 __global__ void __launch_bounds__(kTrdThreads) trd_kernel(const double* __restrict__ H, int p,
                                                           double* __restrict__ refl, double* __restrict__ tau_out,
                                                           double* __restrict__ d_out, double* __restrict__ e_out,
@@ -75,6 +107,9 @@ __global__ void __launch_bounds__(kTrdThreads) trd_kernel(const double* __restri
     ws[0][i] = ws[1][i] = 0.0;
   }
   __syncthreads();
+#ifdef TSK_TRD_PROF
+  long long pf0 = 0, pf1 = 0, pf2 = 0, pc = clock64();
+#endif
   for (int j = 0; j + 2 < p; ++j) {
     const int cur = j & 1, prv = cur ^ 1;
     const double* vp = vs[prv];  // pending update v_{j-1}, w_{j-1} (zero at j = 0), indices >= j
@@ -99,10 +134,10 @@ __global__ void __launch_bounds__(kTrdThreads) trd_kernel(const double* __restri
       ajj = __shfl_sync(0xffffffffu, xi[0], 0);
       double tau = 0.0, beta = alpha, scal = 0.0;
       if (s2 > 0.0) {
-        const double mu = sqrt(fma(alpha, alpha, s2));
+        const double mu = fast_sqrt(fma(alpha, alpha, s2));
         beta = alpha <= 0.0 ? mu : -mu;
-        tau = (beta - alpha) * __drcp_rn(beta);
-        scal = __drcp_rn(alpha - beta);
+        tau = (beta - alpha) * fast_rcp(beta);
+        scal = fast_rcp(alpha - beta);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -121,10 +156,38 @@ __global__ void __launch_bounds__(kTrdThreads) trd_kernel(const double* __restri
       }
     }
     __syncthreads();
+#ifdef TSK_TRD_PROF
+    { const long long c = clock64(); pf0 += c - pc; pc = c; }
+#endif
     const double tau = sc[0];
     const double* v = vs[cur];
     // fused pass: A22 -= vp wp^T + wp vp^T (pending), pv = tau A22 v
-    {
+    if constexpr (kRow) {
+      const int i = j + 1 + (tid >> 2), sg = tid & 3;
+      double acc0 = 0.0, acc1 = 0.0;
+      if (i < p) {
+        const double vpi = vp[i], wpi = wp[i];
+        double* row = A + i * ld;
+        int l = j + 1 + sg;
+        for (; l + 4 < p; l += 8) {
+          const double a0 = row[l] - fma(vpi, wp[l], wpi * vp[l]);
+          const double a1 = row[l + 4] - fma(vpi, wp[l + 4], wpi * vp[l + 4]);
+          row[l] = a0;
+          row[l + 4] = a1;
+          acc0 = fma(a0, v[l], acc0);
+          acc1 = fma(a1, v[l + 4], acc1);
+        }
+        if (l < p) {
+          const double a0 = row[l] - fma(vpi, wp[l], wpi * vp[l]);
+          row[l] = a0;
+          acc0 = fma(a0, v[l], acc0);
+        }
+      }
+      double acc = acc0 + acc1;
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (sg == 0 && i < p) pvs[i] = tau * acc;
+    } else {
       double vpc[KC], wpc[KC], vc[KC];
 #pragma unroll
       for (int c = 0; c < KC; ++c) {
@@ -189,6 +252,9 @@ __global__ void __launch_bounds__(kTrdThreads) trd_kernel(const double* __restri
       }
     }
     __syncthreads();
+#ifdef TSK_TRD_PROF
+    { const long long c = clock64(); pf1 += c - pc; pc = c; }
+#endif
     if (warp == 0) {
       double s = 0.0;
       for (int i = j + 1 + lane; i < p; i += 32) s = fma(pvs[i], v[i], s);
@@ -199,7 +265,13 @@ __global__ void __launch_bounds__(kTrdThreads) trd_kernel(const double* __restri
       if (lane == 0) vs[cur][j] = 0.0;
     }
     __syncthreads();
+#ifdef TSK_TRD_PROF
+    { const long long c = clock64(); pf2 += c - pc; pc = c; }
+#endif
   }
+#ifdef TSK_TRD_PROF
+  if (tid == 0 && blockIdx.y == 0) { trd_prof[0] = pf0; trd_prof[1] = pf1; trd_prof[2] = pf2; trd_prof[3] = p; }
+#endif
   if (tid == 0) {
     if (p >= 3) {
       // the last 2 x 2 block with the pending update of step p - 3
@@ -986,6 +1058,7 @@ tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch,
   static uint64_t attr = 0;
   if (!(attr & device_bit())) {
     cudaFuncSetAttribute(trd_kernel<true, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(trd_kernel<true, 8, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(trd_kernel<true, 16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     cudaFuncSetAttribute(orth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(tev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
@@ -1019,9 +1092,14 @@ tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch,
     ctx->count_launch(2);
   } else if (p <= 128 && getenv("TSK_TRD_REG"))
     trd_reg_kernel<<<g1, kTrdThreads, 0, st>>>(H, p, refl, tau, d, e, hs, wsz);
-  else if (p <= 129)
-    trd_kernel<true, 8, 4><<<g1, kTrdThreads, asmem, st>>>(H, p, refl, tau, d, e, nullptr, hs, wsz);
-  else if (p <= kTrdSmemMaxP)
+  else if (p <= 129) {
+    // the row-parallel pass wins below ~p = 90 (p = 48: 1070 vs 1589 cycles per step, 76: 1394 vs 1950) and
+    // loses above (96: 2614 vs 2249, 128: 4264 vs 2848; its 4-thread rows serialise (p - j) / 4 columns)
+    if (p > 88 || getenv("TSK_TRD_TILE"))
+      trd_kernel<true, 8, 4><<<g1, kTrdThreads, asmem, st>>>(H, p, refl, tau, d, e, nullptr, hs, wsz);
+    else
+      trd_kernel<true, 8, 4, true><<<g1, kTrdThreads, asmem, st>>>(H, p, refl, tau, d, e, nullptr, hs, wsz);
+  } else if (p <= kTrdSmemMaxP)
     trd_kernel<true, 16, 8><<<g1, kTrdThreads, asmem, st>>>(H, p, refl, tau, d, e, nullptr, hs, wsz);
   else
     trd_kernel<false, 16, 8><<<g1, kTrdThreads, 0, st>>>(H, p, refl, tau, d, e, gA, hs, wsz);
@@ -1047,3 +1125,8 @@ tsk_status syev_top(Ctx* ctx, const double* H, int p, int nw, double* W, int ldw
 }
 
 }  // namespace tsk
+#ifdef TSK_TRD_PROF
+extern "C" int tsk_trd_prof_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, tsk::trd_prof, sizeof(long long) * 4) == cudaSuccess ? 0 : -4;
+}
+#endif

@@ -8,6 +8,7 @@ import datagen  # noqa: E402
 import paper_2209_14637_b200 as tsk  # noqa: E402
 
 names = sys.argv[1:] or ["C3", "C4", "C5"]
+opts = {"oversample": int(os.environ["OVERSAMPLE"])} if os.environ.get("OVERSAMPLE") else None
 for name in names:
     c = datagen.CONFIGS[name]
     G = torch.zeros(c.m, c.m, dtype=torch.float64, device="cuda")
@@ -24,7 +25,7 @@ for name in names:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        S, lam, info, st = tsk.sketch_topk(G, c.k)
+        S, lam, info, st = tsk.sketch_topk(G, c.k, opts=opts)
         e1.record()
         torch.cuda.synchronize()
         Sd = S.double()
