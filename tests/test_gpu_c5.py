@@ -2,8 +2,9 @@
 
 The full C5 training stream is 2000 x 64 MB; the oracle's Gram of it takes ~20 min on the host, so
 parity is checked (i) on a reduced stream D_train = 24 (same generator, shapes, k, r) through the
-whole path -- Gram rel-F, sketch Ky Fan deficit / orthonormality, SCW errors -- and (ii) at the full
-C5 matrix shape with D = 64 on sampled Gram entries computed one by one in fp64.  The two-sided
+whole path -- Gram rel-F, sketch Ky Fan deficit / orthonormality, SCW errors -- (ii) at the full
+C5 matrix shape with D = 64 on sampled Gram entries computed one by one in fp64, and (iii) on the full
+2000-frame stream through sampled Gram entries and properties of the sketch that hold at any size.  The two-sided
 entry points are exercised at C5's m, n with k = l = 100."""
 import numpy as np
 import pytest
@@ -65,5 +66,39 @@ def test_c5_two_sided_scw(c5_small):
                      dtype=torch.float32, device="cuda")
     err = tsk.two_sided_scw_error(T, S, W, C5.r).cpu().numpy()
     eo = tucker2.two_sided_scw_errors(T.cpu().numpy(), S.cpu().double().numpy(), W.cpu().double().numpy(), C5.r)
+    fro = np.linalg.norm(T.cpu().double().numpy().reshape(T.shape[0], -1), axis=1)
+    assert np.all(np.abs(err - eo) <= 1e-4 * eo + 1e-6 * fro)
+
+
+def test_c5_full_stream_properties():
+    """C5 at its full size (D_train = 2000 frames of 4096 x 4096, generated and accumulated in chunks of 100
+    as the streaming use does): sampled Gram entries in fp64 from the same frames (one by one, the definition), then the
+    sketch through properties that hold at any size -- Ky Fan deficit against fp64 eigvalsh of the
+    accumulated G, orthonormal rows -- and SCW errors of sampled test matrices against the oracle."""
+    D, ch = C5.D_train, 100
+    G = torch.zeros(C5.m, C5.m, dtype=torch.float64, device="cuda")
+    rng = np.random.default_rng(4)
+    R = np.unique(np.concatenate([rng.choice(C5.m, 14, replace=False), [0, C5.m - 1]]))
+    Rt = torch.tensor(R, device="cuda")
+    Go = np.zeros((len(R), len(R)))
+    for d0 in range(0, D, ch):
+        A = datagen.generate(C5, "train", d0, d0 + ch, device="cuda")
+        tsk.sketch_gram(A, G64=G, accumulate=d0 > 0)
+        Ar = A[:, Rt, :].double().cpu().numpy()
+        Go += np.einsum("dik,djk->ij", Ar, Ar)
+        del A
+    Gg = G[Rt][:, Rt].cpu().numpy()
+    scale = np.sqrt(np.outer(np.diag(Go), np.diag(Go)))
+    assert np.max(np.abs(Gg - Go) / scale) <= 1e-5
+    S, lam, info, st = tsk.sketch_topk(G, C5.k)
+    assert st == 0
+    Sd = S.double()
+    lam_ref = torch.linalg.eigvalsh(G).flip(0)[: C5.k].sum().item()
+    kf = torch.trace(Sd @ G @ Sd.T).item()
+    assert abs(lam_ref - kf) <= 1e-6 * lam_ref
+    assert torch.linalg.norm(Sd @ Sd.T - torch.eye(C5.k, device="cuda", dtype=torch.float64)).item() <= 1e-5
+    T = torch.stack([datagen.generate(C5, "test", i, i + 1, device="cuda")[0] for i in (0, 100, 255)])
+    err = tsk.scw_error(T, S, C5.r).cpu().numpy()
+    eo = oscw.scw_errors(T.cpu().numpy(), S.cpu().double().numpy(), C5.r)
     fro = np.linalg.norm(T.cpu().double().numpy().reshape(T.shape[0], -1), axis=1)
     assert np.all(np.abs(err - eo) <= 1e-4 * eo + 1e-6 * fro)
