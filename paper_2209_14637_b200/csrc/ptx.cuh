@@ -349,4 +349,29 @@ __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
          | ((M >> 4) << 24);  // M
 }
 
+// fp64 reciprocal / square root without IEEE rounding: the MUFU seed (~2^-22) and two Newton steps
+// (quadratic: beyond 2^-53), a dependent chain of ~6 FMAs instead of the correctly rounded library
+// sequences (__drcp_rn, sqrt: ~150-300 cycles each with their special-case branches) -- the Householder
+// step of trd_kernel evaluates one square root and two reciprocals on its critical path.  Finite positive
+// (rcp: nonzero) arguments only.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double fast_sqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * r, r, 0.5);
+  r = fma(r, e, r);
+  e = fma(-h * r, r, 0.5);
+  r = fma(r, e, r);
+  const double s0 = x * r;                 // sqrt(x) to ~1 ulp; one more correction step
+  return fma(fma(-s0, s0, x), 0.5 * r, s0);
+}
+
 }  // namespace tsk

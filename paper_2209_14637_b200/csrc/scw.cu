@@ -105,8 +105,10 @@ __global__ void __launch_bounds__(CT * 4) scw_combine2_kernel(const float* __res
                                                               const double* __restrict__ W,
                                                               const double* __restrict__ mu, int k, int len,
                                                               int nout, int ldw, long long wst,
-                                                              float* __restrict__ Out, int ldo) {
+                                                              float* __restrict__ Out, int ldo,
+                                                              const int* __restrict__ only) {
   constexpr int JT = 64, KC = 16, CG = CT / 4;
+  if (only && only[blockIdx.z] == 0) return;  // error-only path: factors of the dense-marked matrices only
   __shared__ double Ws[KC][CT + 1];
   __shared__ double Is[KC][JT + 1];
   __shared__ double sc[CT];
@@ -169,16 +171,18 @@ __global__ void __launch_bounds__(CT * 4) scw_combine2_kernel(const float* __res
   }
 }
 
-// Out = combination of the k rows of In by W (see scw_combine_kernel), tiled over (64 columns, CT outputs)
+// Out = combination of the k rows of In by W (see scw_combine_kernel), tiled over (64 columns, CT outputs);
+// only (optional, [batch]): matrices with only[b] == 0 are skipped
 template <bool kVt>
 static void launch_combine2(const float* In, const double* W, const double* mu, int k, int len, int nout, int ldw,
-                            long long wst, float* Out, int ldo, int batch, cudaStream_t s) {
+                            long long wst, float* Out, int ldo, int batch, cudaStream_t s,
+                            const int* only = nullptr) {
   if (nout <= 32)
     scw_combine2_kernel<32, kVt><<<dim3((len + 63) / 64, 1, batch), 128, 0, s>>>(In, W, mu, k, len, nout, ldw, wst,
-                                                                                 Out, ldo);
+                                                                                 Out, ldo, only);
   else
     scw_combine2_kernel<64, kVt><<<dim3((len + 63) / 64, (nout + 63) / 64, batch), 256, 0, s>>>(
-        In, W, mu, k, len, nout, ldw, wst, Out, ldo);
+        In, W, mu, k, len, nout, ldw, wst, Out, ldo, only);
 }
 
 static inline size_t combine_smem(int k, int nout) {
@@ -656,23 +660,28 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
       if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k, eigws)) != TSK_OK) return st;
       if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag, eigws)) != TSK_OK) return st;
     }
-    // 5. factors
-    float* Lc = L ? L + (size_t)b0 * m * r : Lw + (size_t)off * m * ldf;
-    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf + (size_t)off * n * ldf;
-    launch_combine2<false>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf, bc, s);
-    launch_combine2<false>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf, bc, s);
-    ctx->count_launch(2);
-    if (sigma) {
-      scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
-      ctx->count_launch();
-    }
-    // 6. errors: Pythagorean identity, dense residual for the marked matrices (all of them with
-    // TSK_SCW_DENSE); the error path always has pitch-aligned workspace factors
+    // 5. errors by the Pythagorean identity first: on the error-only path (no caller factors) the
+    // factors are then formed only for the matrices it marks for the dense residual
     if (pyth) {
       scw_err_pyth_kernel<<<nb((long long)bc * 32, 256), 256, 0, s>>>(sq_all + off * sq_per, sq_per, sig2, k, r, bc,
                                                                       pyth_tau, err + b0, dense_all + off);
       ctx->count_launch();
     }
+    // 6. factors (all matrices when the caller asked for them)
+    const int* fmask = (pyth && !L && !R) ? dense_all + off : nullptr;
+    float* Lc = L ? L + (size_t)b0 * m * r : Lw + (size_t)off * m * ldf;
+    float* Rc = R ? R + (size_t)b0 * n * r : Lw + (size_t)chunk * m * ldf + (size_t)off * n * ldf;
+    if (L || R || err) {
+      launch_combine2<false>(Zt, W2, nullptr, k, m, r, k, (long long)kk, Lc, ldf, bc, s, fmask);
+      launch_combine2<false>(Vt, W2, nullptr, k, n, r, k, (long long)kk, Rc, ldf, bc, s, fmask);
+      ctx->count_launch(2);
+    }
+    if (sigma) {
+      scw_sigma_kernel<<<nb((long long)bc * r, 256), 256, 0, s>>>(sig2, k, r, bc, sigma + (size_t)b0 * r);
+      ctx->count_launch();
+    }
+    // 7. dense residual for the marked matrices (all of them with TSK_SCW_DENSE); the error path always
+    // has pitch-aligned workspace factors
     if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part + (size_t)off * tiles, err + b0,
                                  pyth ? dense_all + off : nullptr)) != TSK_OK)
       return st;

@@ -1,6 +1,7 @@
 """Eigensolver (sketch_topk) on the C3 / C4 / C5 training Grams: time, products, Ky Fan deficit against
 fp64 eigvalsh of the same Gram (total and excluding a locked dominant pair).  TSK_EIG_TRACE=1 for the
-per-iteration lines.  python scripts/eig_bench.py [C3 C4 C5]"""
+per-iteration lines; PROFILE=1 brackets the last repetition with cudaProfilerStart/Stop (ncu
+--profile-from-start off).  python scripts/eig_bench.py [C3 C4 C5]"""
 import os, sys, time
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -24,10 +25,15 @@ for name in names:
     for rep in range(3):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        prof = rep == 2 and os.environ.get("PROFILE")
+        if prof:
+            torch.cuda.profiler.start()
         e0.record()
         S, lam, info, st = tsk.sketch_topk(G, c.k, opts=opts)
         e1.record()
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         Sd = S.double()
         kf = torch.trace(Sd @ G @ Sd.T).item()
         tot = w[: c.k].sum().item()

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out/r02e
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r02e/pytest_gpu.log 2>&1; tail -3 gpurun_out/r02e/pytest_gpu.log
+timeout 400 python bench.py --e2e-steps 0 --no-cpu-baseline > gpurun_out/r02e/bench.json 2> gpurun_out/r02e/bench.err
+python -c "import json;d=json.load(open('gpurun_out/r02e/bench.json'));print(d['value'],d['ms_per_step'],d['phases_ms'],d['clocks'])"
