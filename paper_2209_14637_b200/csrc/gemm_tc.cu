@@ -70,6 +70,7 @@ struct GemmArgs {
   long long dstride;
   int ldd;
   const int* only;   // batch mode: problems b with only[b] == 0 are skipped by every role (null: all)
+  const int* only_any;  // optional device count of problems with only[b] != 0: 0 => the whole grid exits at once
   double* sq_part;   // TS kernel: [U][8] fp64 sums of the squared X elements of each unit (transform warps)
 };
 
@@ -417,6 +418,8 @@ template <bool kN64, bool kYT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_ts_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                           const GemmArgs a) {
+  // nothing to compute (e.g. no matrix marked for SCW's dense residual): leave before any setup
+  if (a.only_any && *a.only_any == 0) return;
   constexpr int RS = ts_raw_stages<kN64, kYT>();          // raw ring depth
   constexpr int RSB = ts_raw_stage_bytes<kN64, kYT>();    // raw stage: [X | Y] (Y = bn x 32 fp32)
   constexpr int LB = ts_lo_stage_bytes<kN64, kYT>();      // lo stage: [L_Y] or [H_Y | L_Y]
@@ -1095,6 +1098,7 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.res_ld = p.res_ld;
   a.res_part = p.res_part;
   a.only = p.only;
+  a.only_any = p.only_any;
   a.sq_part = p.sq_part;
   if ((p.only || p.sq_part) && !p.batch) return TSK_EINVAL;
   a.dout = p.dout;

@@ -220,8 +220,10 @@ __global__ void scw_err_reduce_kernel(const double* __restrict__ part, int tiles
 // order), sigma_i^2 are the eigenvalues of (AV)^T AV.  The subtraction cancels when the error is small
 // against ||A||: below tau ||A||^2 (or a non-finite value) the matrix is marked for the dense residual
 // ||A - L R^T|| (dense[b] = 1), which then overwrites err[b].  One warp per matrix, fixed-order sums.
+// ndense (zeroed by the caller) counts the marked matrices: the residual launch exits at once when none is.
 __global__ void scw_err_pyth_kernel(const double* __restrict__ sq, int per, const double* __restrict__ sig2, int k,
-                                    int r, long long B, double tau, double* __restrict__ err, int* __restrict__ dense) {
+                                    int r, long long B, double tau, double* __restrict__ err, int* __restrict__ dense,
+                                    int* __restrict__ ndense) {
   const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -236,6 +238,7 @@ __global__ void scw_err_pyth_kernel(const double* __restrict__ sq, int per, cons
     const bool need = !(e2 >= tau * s) || !(s < INFINITY);
     err[b] = need ? 0.0 : sqrt(e2);
     dense[b] = need ? 1 : 0;
+    if (need) atomicAdd(ndense, 1);
   }
 }
 
@@ -307,7 +310,102 @@ __global__ void __launch_bounds__(256) gram_rows_tiled_kernel(const float* __res
   }
 }
 
+// ---------------------------------------------------------------- C = X X^T for k <= 64 (round 2)
+// The symmetric Gram of SCW's k x len row blocks (B = S A_b and (A_b V)^T): one 2-CTA cluster per matrix,
+// each CTA one half of len; 136 threads own the 4 x 4 micro-tiles of the lower triangle of the padded
+// 64 x 64 result (thread t -> micro-tile row ty >= column tx), reading two 16-byte pairs of the
+// transposed fp64 chunk per K index for 16 DFMA -- half the products of the full 64 x 64 tile of
+// gram_rows_tiled_kernel and 2 CTAs per matrix (500 CTAs at C4 instead of 250 on 148 SMs).  CTA 1 adds
+// its partial into CTA 0's over DSMEM (fixed order: deterministic), CTA 0 writes both triangles.
+constexpr int kGsThreads = 160, kGsKC = 32, kGsP = 66;  // 136 working threads; chunk pitch 66 doubles
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGsThreads, 4)
+    gram_rows_sym_kernel(const float* __restrict__ X, int k, int len, double* __restrict__ C) {
+  __shared__ __align__(16) double xs[kGsKC][kGsP];
+  __shared__ __align__(16) double part[136][16];
+  const int b = blockIdx.x >> 1;
+  const unsigned rank = cluster_ctarank();
+  const int tid = threadIdx.x;
+  // micro-tile of thread t: row block ty, column block tx <= ty (t = ty (ty + 1) / 2 + tx)
+  int ty = (int)((sqrtf(8.0f * (float)tid + 1.0f) - 1.0f) * 0.5f);
+  while (ty * (ty + 1) / 2 > tid) --ty;
+  while ((ty + 1) * (ty + 2) / 2 <= tid) ++ty;
+  const int tx = tid - ty * (ty + 1) / 2;
+  const bool work = tid < 136;
+  const int half = ((len + 2 * kGsKC - 1) / (2 * kGsKC)) * kGsKC;  // CTA 0: [0, half), CTA 1: [half, len)
+  const int j0 = rank == 0 ? 0 : half, j1 = rank == 0 ? min(half, len) : len;
+  const float* Xb = X + (size_t)b * k * len;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  // fill: item e of a chunk = (column kk = e % 32, row group g = e / 32): four rows 4g .. 4g + 3 of one
+  // column, read as four coalesced 128-B warp loads and stored as two 16-byte pairs of the transposed
+  // chunk (a row-strided 8-byte transpose store was 4-way bank-conflicted: 40 % excess wavefronts)
+  constexpr int kItems = 16 * kGsKC, kPer = (kItems + kGsThreads - 1) / kGsThreads;  // 512 items, 4 per thread
+  // no register prefetch: the loads of one CTA overlap the products of the other three on its SM
+  for (int jc = j0; jc < j1; jc += kGsKC) {
+    __syncthreads();  // the previous chunk is consumed
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = tid + t * kGsThreads, kk = e & 31, g = e >> 5;
+      if (e < kItems) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int r = 4 * g + u;
+          v[u] = (r < k && jc + kk < j1) ? __ldg(Xb + (size_t)r * len + jc + kk) : 0.0f;
+        }
+        *reinterpret_cast<double2*>(&xs[kk][4 * g]) = make_double2((double)v[0], (double)v[1]);
+        *reinterpret_cast<double2*>(&xs[kk][4 * g + 2]) = make_double2((double)v[2], (double)v[3]);
+      }
+    }
+    __syncthreads();
+    if (work) {
+#pragma unroll 8
+      for (int kk = 0; kk < kGsKC; ++kk) {
+        const double2 a01 = *reinterpret_cast<const double2*>(&xs[kk][4 * ty]);
+        const double2 a23 = *reinterpret_cast<const double2*>(&xs[kk][4 * ty + 2]);
+        const double2 c01 = *reinterpret_cast<const double2*>(&xs[kk][4 * tx]);
+        const double2 c23 = *reinterpret_cast<const double2*>(&xs[kk][4 * tx + 2]);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y}, cv[4] = {c01.x, c01.y, c23.x, c23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], cv[v], acc[u][v]);
+      }
+    }
+  }
+  if (work && rank == 1) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) part[tid][u * 4 + v] = acc[u][v];
+  }
+  cluster_sync();
+  if (work && rank == 0) {
+    const uint32_t rp = mapa_shared(smem_u32(&part[tid][0]), 1);
+    double* Cb = C + (size_t)b * k * k;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = 4 * ty + u, j = 4 * tx + v;
+        const double val = acc[u][v] + ld_dsmem_f64(rp + (uint32_t)(u * 4 + v) * 8u);
+        if (i < k && j < k && j <= i) {
+          Cb[(size_t)i * k + j] = val;
+          Cb[(size_t)j * k + i] = val;
+        }
+      }
+  }
+  cluster_sync();  // CTA 1's partial stays readable until CTA 0 is done
+}
+
 static void launch_gram_rows_tiled(const float* X, int k, int len, int batch, double* C, cudaStream_t s) {
+  if (k <= 64 && batch > 0) {
+    gram_rows_sym_kernel<<<2 * batch, kGsThreads, 0, s>>>(X, k, len, C);
+    return;
+  }
   const int nt = (k + 63) / 64;
   gram_rows_tiled_kernel<<<dim3(nt * nt, batch), 256, 0, s>>>(X, k, len, C, nullptr, 0);
 }
@@ -468,7 +566,8 @@ static inline unsigned nb(long long n, int t) { return (unsigned)((n + t - 1) / 
 // (3xTF32, K = r, one 128 x 128 tile per unit) with the residual epilogue of gemm_tc.cu reading
 // the A tile and reducing (a - s)^2 in fp64; fixed-order reduction of the per-warp partials.
 static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, const float* Lc, const float* Rc,
-                              int r, int ldf, double* part, double* err, const int* only = nullptr) {
+                              int r, int ldf, double* part, double* err, const int* only = nullptr,
+                              const int* only_any = nullptr) {
   GemmProblem gp;
   gp.X = Lc;
   gp.Y = Rc;
@@ -487,6 +586,7 @@ static tsk_status residual_tc(Ctx* ctx, const float* Ac, int bc, int m, int n, c
   gp.res_ld = n;
   gp.res_part = part;
   gp.only = only;
+  gp.only_any = only_any;
   tsk_status st = gemm_tf32x3(ctx, gp);
   if (st != TSK_OK) return st;
   const int per = (int)(nb(m, 128) * nb(n, 128)) * 8;  // partials per matrix
@@ -527,7 +627,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   // matrix) and the dense-residual marks of the Pythagorean error path
   const int sq_per = (int)nb(n, 128) * 8;
   double* part = reinterpret_cast<double*>(
-      ctx->workspace(WS_SCW_5, chunk * ((size_t)tiles + sq_per) * 8 + chunk * 4 + 64));
+      ctx->workspace(WS_SCW_5, chunk * ((size_t)tiles + sq_per) * 8 + chunk * 8 + 64));
   if (!Bm_all || !Vt_all || !Zt_all || !small || !Lw || !part) return TSK_ENOMEM;
   double* sq_all = part + chunk * tiles;
   // eigensolver scratch per matrix: the parts run concurrently on different streams
@@ -535,6 +635,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
   double* eigws_all = reinterpret_cast<double*>(ctx->workspace(WS_SCW_EIG, (size_t)chunk * eig_ws * 8));
   if (!eigws_all) return TSK_ENOMEM;
   int* dense_all = reinterpret_cast<int*>(sq_all + chunk * sq_per);
+  int* ndense_all = dense_all + chunk;  // one counter per part (indexed by the part's offset)
   // Pythagorean error path (reading c17) unless TSK_SCW_DENSE; tau: the cancellation threshold
   static const bool force_dense = getenv("TSK_SCW_DENSE") != nullptr;
   static const double env_tau = getenv("TSK_SCW_PYTH_TAU") ? atof(getenv("TSK_SCW_PYTH_TAU")) : kScwPythTau;
@@ -654,18 +755,28 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     // wanted eigenvalues form an unresolved cluster (e.g. rank(A) < r: a null cluster among them) sets the
     // flag, and the Jacobi eigensolver -- enqueued behind it, gated on the flag on the device -- redoes the
     // batch (no host round trip)
-    {
-      int* gflag = reinterpret_cast<int*>(small + chunk * (4 * kk + 2 * k)) + off;
-      cudaMemsetAsync(gflag, 0, sizeof(int), s);
-      if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k, eigws)) != TSK_OK) return st;
-      if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag, eigws)) != TSK_OK) return st;
-    }
+    // on the error-only path the eigenvalues come first (bisection only) and the vectors -- needed for the
+    // rank-r factors of the dense residual -- only for the matrices the Pythagorean step marks
+    const bool vals_first = pyth && !L && !R;
+    int* gflag = reinterpret_cast<int*>(small + chunk * (4 * kk + 2 * k)) + off;
+    cudaMemsetAsync(gflag, 0, sizeof(int), s);
+    if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k, eigws, vals_first ? 1 : 0)) != TSK_OK)
+      return st;
+    if (!vals_first && (st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag, eigws)) != TSK_OK)
+      return st;
     // 5. errors by the Pythagorean identity first: on the error-only path (no caller factors) the
     // factors are then formed only for the matrices it marks for the dense residual
     if (pyth) {
+      cudaMemsetAsync(ndense_all + off, 0, sizeof(int), s);
       scw_err_pyth_kernel<<<nb((long long)bc * 32, 256), 256, 0, s>>>(sq_all + off * sq_per, sq_per, sig2, k, r, bc,
-                                                                      pyth_tau, err + b0, dense_all + off);
+                                                                      pyth_tau, err + b0, dense_all + off,
+                                                                      ndense_all + off);
       ctx->count_launch();
+    }
+    if (vals_first) {
+      if ((st = syev_top_batched(ctx, H, k, r, bc, W2, k, sig2, gflag, 1e-9, k, eigws, 2, dense_all + off)) != TSK_OK)
+        return st;
+      if ((st = jacobi_eig_batched(ctx, H, k, bc, W2, sig2, nullptr, 1e-10, gflag, eigws)) != TSK_OK) return st;
     }
     // 6. factors (all matrices when the caller asked for them)
     const int* fmask = (pyth && !L && !R) ? dense_all + off : nullptr;
@@ -683,7 +794,7 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     // 7. dense residual for the marked matrices (all of them with TSK_SCW_DENSE); the error path always
     // has pitch-aligned workspace factors
     if (err && (st = residual_tc(ctx, Ac, bc, m, n, Lc, Rc, r, ldf, part + (size_t)off * tiles, err + b0,
-                                 pyth ? dense_all + off : nullptr)) != TSK_OK)
+                                 pyth ? dense_all + off : nullptr, pyth ? ndense_all + off : nullptr)) != TSK_OK)
       return st;
     if ((st = launch_status("scw")) != TSK_OK) return st;
     return TSK_OK;

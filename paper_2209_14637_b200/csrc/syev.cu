@@ -818,9 +818,11 @@ __global__ void __launch_bounds__(1024) tev_cta_kernel(const double* __restrict_
                                                        const double* __restrict__ tau_g,
                                                        const double* __restrict__ refl,
                                                        double* __restrict__ W, int ldw, double* __restrict__ lam,
-                                                       long long wsz, long long wstride, long long lstride) {
+                                                       long long wsz, long long wstride, long long lstride, int vmode,
+                                                       const int* __restrict__ only) {
   extern __shared__ __align__(16) double tc_sm[];
   const long long b = blockIdx.x;
+  if (vmode == 2 && only[b] == 0) return;  // vectors only for the problems the caller marks
   d_g += b * wsz;
   e_g += b * wsz;
   tau_g += b * wsz;
@@ -834,7 +836,8 @@ __global__ void __launch_bounds__(1024) tev_cta_kernel(const double* __restrict_
   double* e = e2 + p;                               // [p]
   double* tau = e + p;                              // [p]
   double* scratch = tau + p;                        // per warp: Dp, Lp, Dm, Um, z [5][p]
-  for (int x = tid; x < max(p - 2, 0) * p; x += blockDim.x) R[x] = refl[x];
+  if (vmode != 1)
+    for (int x = tid; x < max(p - 2, 0) * p; x += blockDim.x) R[x] = refl[x];
   for (int k = tid; k < p; k += blockDim.x) {
     d[k] = d_g[k];
     const double ek = k + 1 < p ? e_g[k] : 0.0;
@@ -881,6 +884,10 @@ __global__ void __launch_bounds__(1024) tev_cta_kernel(const double* __restrict_
       hi = fmin(hi, nhi);
     }
     const double lm = 0.5 * (lo + hi);
+    if (vmode == 1) {  // eigenvalues only (SCW's error path needs sum_{i<r} sigma_i^2, not the vectors)
+      if (lane == 0) lam[i] = lm;
+      continue;
+    }
     if (lane == 0) {
       double D = d[0] - lm;
       Dp[0] = D;
@@ -953,7 +960,9 @@ __global__ void __launch_bounds__(1024) tev_cta_kernel(const double* __restrict_
 
 // flag[0] = 1 if max_{a,b < nw} |(W^T W)_ab - delta_ab| > tol  (W [p][ldw], columns 0..nw-1)
 __global__ void __launch_bounds__(512) orth_kernel(const double* __restrict__ W, int p, int nw, int ldw, double tol,
-                                                   int* __restrict__ flag, int use_smem, long long wstride) {
+                                                   int* __restrict__ flag, int use_smem, long long wstride,
+                                                   const int* __restrict__ only) {
+  if (only && only[blockIdx.y] == 0) return;
   W += (long long)blockIdx.y * wstride;
   extern __shared__ double osm[];
   __shared__ double red[16];
@@ -1006,7 +1015,7 @@ long long syev_ws_doubles(int p) {
 }
 
 tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch, double* W, int ldw, double* lam,
-                            int* flag, double orth_tol, long long lstride, double* ws) {
+                            int* flag, double orth_tol, long long lstride, double* ws, int vmode, const int* only) {
   if (p < 1 || p > 256 || nw < 1 || nw > p || ldw < nw || batch < 0) return TSK_EINVAL;
   if (lstride <= 0) lstride = nw;
   if (batch == 0) return TSK_OK;
@@ -1030,6 +1039,9 @@ tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch,
     }
     return cudaPeekAtLastError() == cudaSuccess ? TSK_OK : TSK_ECUDA;
   }
+  const bool small = p <= 128 && batch >= 8 && !getenv("TSK_SYEV_CTA");
+  if (!small && vmode == 2) return TSK_OK;  // the vectors came with the values (vmode 1 == 0 there)
+  if (!small) only = nullptr;
   static uint64_t attr = 0;
   if (!(attr & device_bit())) {
     cudaFuncSetAttribute(trd_kernel<true, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
@@ -1045,26 +1057,35 @@ tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch,
   const size_t asmem = (size_t)p * (p + 1) * sizeof(double);
   const dim3 g1(1, batch);
   const long long hs = (long long)pp;
-  // many problems: a warp per tridiagonalisation and a CTA per problem's eigenpairs keep every SM busy
-  // with independent latency chains (SCW: 250 Grams per launch, 0.94 -> ~0.5 ms); a single problem (the
-  // eigensolver's Rayleigh-Ritz matrix) is faster on the whole-CTA kernels (one warp takes 490 us at p = 60)
-  const bool small = p <= 128 && batch >= 8 && !getenv("TSK_SYEV_CTA");
+  // many problems: a CTA per tridiagonalisation (p <= 88; a warp per problem above) and a CTA per
+  // problem's eigenpairs keep every SM busy with independent latency chains (SCW: 250 Grams per launch);
+  // a single problem (the eigensolver's Rayleigh-Ritz matrix) takes the per-eigenpair CTAs of tev_kernel
   if (small) {
-    // warp per problem: as many problems per CTA as fit 200 KB of shared memory (<= 8)
+    // warp-per-problem geometry: as many problems per CTA as fit 200 KB of shared memory (<= 8)
     const size_t per = ((size_t)p * (p | 1) + 2 * 128) * sizeof(double);
     // spread the problems over the SMs first (each warp is one latency chain), then stack them
     const int want = (batch + ctx->num_sms - 1) / ctx->num_sms;
     const int wpb = (int)std::max<size_t>(1, std::min<size_t>(std::min(8, want), (200 * 1024) / per));
     const int nblk = (batch + wpb - 1) / wpb;
-    trd_warp_kernel<<<nblk, 32 * wpb, per * wpb, st>>>(H, p, batch, refl, tau, d, e, hs, wsz);
+    if (vmode != 2) {
+      // a CTA per tridiagonalisation up to p = 88 (row-parallel pass; C4 SCW, p = 60, 250 problems: 118 us
+      // against 232 us for a warp per problem -- 250 one-warp latency chains leave the SMs mostly idle)
+      static const bool warp_only = getenv("TSK_SYEV_TRD_WARP") != nullptr;
+      if (!warp_only && p <= 88)
+        trd_kernel<true, 8, 4, true><<<g1, kTrdThreads, asmem, st>>>(H, p, refl, tau, d, e, nullptr, hs, wsz);
+      else
+        trd_warp_kernel<<<nblk, 32 * wpb, per * wpb, st>>>(H, p, batch, refl, tau, d, e, hs, wsz);
+      ctx->count_launch();
+    }
     const size_t fixed = ((size_t)std::max(p - 2, 0) * p + 4 * (size_t)p) * sizeof(double);
     const size_t per_warp = (size_t)5 * p * sizeof(double);
     const int fit = (int)(((size_t)200 * 1024 - fixed) / per_warp);
     const int warps = std::max(1, std::min(std::min(32, nw), fit));
     const size_t tsm = fixed + (size_t)warps * per_warp;
     tev_cta_kernel<<<batch, 32 * warps, tsm, st>>>(d, e, p, nw, tau, refl, W, ldw, lam, wsz, p * (long long)ldw,
-                                                   lstride);
-    ctx->count_launch(2);
+                                                   lstride, vmode, only);
+    ctx->count_launch();
+    if (vmode == 1) return launch_status("syev_top (values)");
   } else if (p <= 128 && getenv("TSK_TRD_REG"))
     trd_reg_kernel<<<g1, kTrdThreads, 0, st>>>(H, p, refl, tau, d, e, hs, wsz);
   else if (p <= 129) {
@@ -1088,7 +1109,8 @@ tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch,
   if (flag) {
     const size_t wsm = (size_t)(p | 1) * nw * sizeof(double);
     const int use_smem = wsm <= 220 * 1024;
-    orth_kernel<<<dim3(1, batch), 512, use_smem ? wsm : 0, st>>>(W, p, nw, ldw, orth_tol, flag, use_smem, wstride);
+    orth_kernel<<<dim3(1, batch), 512, use_smem ? wsm : 0, st>>>(W, p, nw, ldw, orth_tol, flag, use_smem, wstride,
+                                                                  only);
     ctx->count_launch();
   }
   return launch_status("syev_top");

@@ -195,6 +195,7 @@ struct GemmProblem {
   double* res_part = nullptr;
   // batch mode: only problems b with only[b] != 0 are computed (the others' outputs are not written)
   const int* only = nullptr;
+  const int* only_any = nullptr;  // optional: device count of nonzero only[b] (0: the launch does nothing)
   // TS kernel, batch mode: sq_part[unit][8] = fp64 sums of the squared X elements each unit reads
   // (unit u of problem b: u = b * tiles + tile; every X element of a problem in exactly one unit when N
   // fits one column block)
@@ -240,8 +241,12 @@ tsk_status syev_top(Ctx* ctx, const double* H, int p, int nw, double* W, int ldw
 // the same for a batch: H [batch][p][p], W [batch][p][ldw], lam [batch][nw]; flag set if any problem fails
 // ws (optional): caller-owned scratch of syev_ws_doubles(p) doubles per problem (else the ctx's WS_SYEV,
 // which two concurrent calls on different streams must not share)
+// vmode 1: eigenvalues only (tridiagonalisation + bisection; no vectors, no orthogonality flag); vmode 2: the
+// vectors (and values) of the problems with only[b] != 0, reusing the tridiagonalisation of a vmode-1 call
+// on the same ws (batched small-p path; elsewhere vmode 1 computes everything and vmode 2 does nothing)
 tsk_status syev_top_batched(Ctx* ctx, const double* H, int p, int nw, int batch, double* W, int ldw, double* lam,
-                            int* flag, double orth_tol, long long lstride = 0, double* ws = nullptr);
+                            int* flag, double orth_tol, long long lstride = 0, double* ws = nullptr, int vmode = 0,
+                            const int* only = nullptr);
 long long syev_ws_doubles(int p);
 
 // batched symmetric PSD eigensolver (one-sided Jacobi), jacobi.cu
