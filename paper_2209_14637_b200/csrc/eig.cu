@@ -1087,7 +1087,8 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     if (b > a && xmax > 1.0 + 1e-12) {
       // T_d(x) ~ exp(d acosh x) / 2 <= R: R = 1e4 on the random first block (its columns carry O(1)
       // components along the top eigenvectors), 1e7 once the block holds Ritz vectors
-      const double R = (outer == 0 ? 1e4 : 1e7) * range_cut;
+      static const double range = getenv("TSK_EIG_RANGE") ? atof(getenv("TSK_EIG_RANGE")) : 1e7;
+      const double R = (outer == 0 ? 1e4 : range) * range_cut;
       d = (int)std::floor(std::log(2.0 * std::max(R, 10.0)) / std::acosh(xmax));
       d = std::max(1, std::min(d, opt.cheb_degree > 0 ? opt.cheb_degree : 40));
     }

@@ -680,8 +680,15 @@ tsk_status gram_pair(Ctx* ctx, const GemmProblem& p) {
   a.cps = cps;
   // chain / fold / lag arrive in chunks (GemmProblem units); the kernel counts stages of kZ chunks
   a.chain = p.chain > 0 ? p.chain : 4;
-  a.fold = p.fold > 0 ? p.fold : 64;
+  // fold every 1024 chains (round 2; was 64): the uncoalesced fp64 L2 reductions of a fold cost ~6 % of
+  // the C4 launch at 64 (23.5 -> ~22.0 ms, scripts/gram_fold.py), while the Gram error is unchanged
+  // (2.72e-6 rel-F at C2-C4 for every fold from 64 to one per unit: it is the tensor core's truncating
+  // accumulation within a chain, not the round-to-nearest fp32 register sums, that sets it)
+  a.fold = p.fold > 0 ? p.fold : 1024;
   a.lag = p.lag >= 0 ? (p.lag + kZ - 1) / kZ : 64 / kZ;
+  // developer overrides (scripts/gram_pair_time.py sweeps)
+  if (const char* ev = getenv("TSK_PAIR_FOLD")) a.fold = std::max(1, atoi(ev));
+  if (const char* ev = getenv("TSK_PAIR_LAG")) a.lag = std::max(1, (atoi(ev) + kZ - 1) / kZ);
   a.part = part;
   a.progress = prog;
   // diagnostics only (developer experiments, scripts/gram_pair_*.py): TSK_PAIR_DIAG bit 0 = skip
