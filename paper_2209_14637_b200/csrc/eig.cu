@@ -200,6 +200,15 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int lds, int c0
   dst[(size_t)i * ldd + d0 + c] = src[(size_t)i * lds + c0 + c];
 }
 
+// dst[i][d0 + c] -= src[i][c]  (m x nc)
+__global__ void sub_cols_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd, int d0,
+                                int m, int nc) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)m * nc) return;
+  const int i = (int)(idx / nc), c = (int)(idx % nc);
+  dst[(size_t)i * ldd + d0 + c] -= src[(size_t)i * lds + c];
+}
+
 // one CholQR pass Q = Y R^{-1}: C = Y^T Y (fp64), R^{-1} from one-CTA Cholesky + inverse, Q = Y R^{-1}
 // (parallel fp64 GEMM); for large blocks (p > 116) the row-parallel TRSM path is used instead.
 static tsk_status cholqr_pass(Ctx* ctx, const double* Y, double* Q, int m, int p, double* C, double* R, int* flag) {
@@ -358,6 +367,146 @@ __global__ void __launch_bounds__(kG2Threads) gq2_f64_kernel(const double* __res
   }
 }
 
+// Tensor-core variant (fp64 mma.sync m8n8k4, DMMA): the same tiles, ring and epilogue; warp w takes the
+// k4-step w of every 32-deep chunk, two 8-row A fragments and NB 8-column B fragments per step feed
+// 2 NB DMMAs (256 FMA each) -- 7 shared loads per 2560 FMA where the DFMA loop above issues 36 loads
+// and 80 DFMAs for the same work.  Shared layouts padded for conflict-free fragment loads (G rows pitch
+// 36, Y rows pitch = BN rounded up to 12 mod 16).
+template <int NB>
+struct Gq3Geom {
+  static constexpr int BN = 8 * NB;
+  static constexpr int BNP = BN + ((12 - BN % 16) + 16) % 16;  // BNP % 16 == 12
+  static constexpr int GP = 36;
+  static constexpr int SG = kG2BM * GP;
+  static constexpr int SS = SG + kG2KC * BNP;
+};
+template <int NB>
+__global__ void __launch_bounds__(kG2Threads) gq3_f64_kernel(const double* __restrict__ G, int m, int ldg,
+                                                             const double* __restrict__ Y,
+                                                             const double* __restrict__ Yp, int q, int ldy,
+                                                             double alpha, double beta, double gamma,
+                                                             double* __restrict__ Out) {
+  using Geo = Gq3Geom<NB>;
+  constexpr int BN = Geo::BN, BNP = Geo::BNP, GP = Geo::GP, SG = Geo::SG, SS = Geo::SS;
+  extern __shared__ __align__(16) double g3_sm[];
+  const int i0 = blockIdx.x * kG2BM, c0 = blockIdx.y * BN;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nch = (m + kG2KC - 1) / kG2KC;
+  constexpr int NGU = (kG2BM * kG2KC + kG2Threads - 1) / kG2Threads;
+  constexpr int NYU = (kG2KC * BN + kG2Threads - 1) / kG2Threads;
+  const double* gsrc[NGU];
+  int gdst[NGU], gkk[NGU];
+  bool gok[NGU];
+#pragma unroll
+  for (int u = 0; u < NGU; ++u) {
+    const int e = tid + u * kG2Threads, r = e / kG2KC, kk = e % kG2KC;
+    gok[u] = e < kG2BM * kG2KC && i0 + r < m;
+    gsrc[u] = gok[u] ? G + (size_t)(i0 + r) * ldg + kk : G;
+    gdst[u] = r * GP + kk;
+    gkk[u] = kk;
+  }
+  const double* ysrc[NYU];
+  int ydst[NYU], ykk[NYU];
+  bool yok[NYU];
+#pragma unroll
+  for (int u = 0; u < NYU; ++u) {
+    const int e = tid + u * kG2Threads, kk = e / BN, c = e % BN;
+    yok[u] = e < kG2KC * BN && c0 + c < q;
+    ysrc[u] = yok[u] ? Y + (size_t)kk * ldy + c0 + c : Y;
+    ydst[u] = kk * BNP + c;
+    ykk[u] = kk;
+  }
+  auto load = [&](int st, int ch) {
+    double* Gs = g3_sm + st * SS;
+    double* Ys = Gs + SG;
+    const int k0 = ch * kG2KC;
+    const size_t yoff = (size_t)k0 * ldy;
+#pragma unroll
+    for (int u = 0; u < NGU; ++u) {
+      if (tid + u * kG2Threads < kG2BM * kG2KC) {
+        const bool ok = gok[u] && k0 + gkk[u] < m;
+        cp_async8(Gs + gdst[u], ok ? gsrc[u] + k0 : G, ok);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NYU; ++u) {
+      if (tid + u * kG2Threads < kG2KC * BN) {
+        const bool ok = yok[u] && k0 + ykk[u] < m;
+        cp_async8(Ys + ydst[u], ok ? ysrc[u] + yoff : Y, ok);
+      }
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < kG2Stages - 1; ++st) {
+    if (st < nch) load(st, st);
+    cp_async_commit();
+  }
+  double acc[2][NB][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / column (A) and column / row (B)
+  for (int ch = 0; ch < nch; ++ch) {
+    cp_async_wait<kG2Stages - 2>();
+    __syncthreads();
+    if (ch + kG2Stages - 1 < nch) load((ch + kG2Stages - 1) % kG2Stages, ch + kG2Stages - 1);
+    cp_async_commit();
+    const double* Gs = g3_sm + (ch % kG2Stages) * SS;
+    const double* Ys = Gs + SG;
+    const int kk = 4 * w + fk;
+    const double a0 = Gs[fr * GP + kk], a1 = Gs[(fr + 8) * GP + kk];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double bv = Ys[kk * BNP + 8 * b + fr];
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[0][b][0]), "+d"(acc[0][b][1]) : "d"(a0), "d"(bv));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[1][b][0]), "+d"(acc[1][b][1]) : "d"(a1), "d"(bv));
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  double* red = g3_sm;  // [8 warps][16][BN]
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      double* rp = red + (w * kG2BM + 8 * a + fr) * BN + 8 * b + 2 * fk;
+      rp[0] = acc[a][b][0];
+      rp[1] = acc[a][b][1];
+    }
+  __syncthreads();
+  for (int e = tid; e < kG2BM * BN; e += kG2Threads) {
+    const int r = e / BN, c = e % BN;
+    const int row = i0 + r, col = c0 + c;
+    if (row >= m || col >= q) continue;
+    double sacc = 0.0;
+#pragma unroll
+    for (int t = 0; t < kG2Warps; ++t) sacc += red[t * kG2BM * BN + e];
+    double v = alpha * sacc;
+    if (beta != 0.0) v = fma(beta, Y[(size_t)row * ldy + col], v);
+    if (gamma != 0.0) v = fma(gamma, Yp[(size_t)row * ldy + col], v);
+    Out[(size_t)row * ldy + col] = v;
+  }
+}
+
+template <int NB>
+static cudaError_t launch_gq3(int ct, cudaStream_t s, const double* G, int m, const double* Y, const double* Yp, int q,
+                              int ldy, double alpha, double beta, double gamma, double* Out) {
+  using Geo = Gq3Geom<NB>;
+  const size_t ring = (size_t)kG2Stages * Geo::SS * sizeof(double);
+  const size_t smem = std::max(ring, (size_t)kG2Warps * kG2BM * Geo::BN * sizeof(double));
+  static uint64_t attr = 0;
+  if (!(attr & device_bit())) {
+    cudaFuncSetAttribute(gq3_f64_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr |= device_bit();
+  }
+  gq3_f64_kernel<NB><<<dim3((m + kG2BM - 1) / kG2BM, ct), kG2Threads, smem, s>>>(G, m, m, Y, Yp, q, ldy, alpha, beta,
+                                                                                  gamma, Out);
+  return cudaGetLastError();
+}
+
 template <int NB>
 static cudaError_t launch_gq2(int ct, cudaStream_t s, const double* G, int m, const double* Y, const double* Yp, int q,
                               int ldy, double alpha, double beta, double gamma, double* Out) {
@@ -383,7 +532,19 @@ static tsk_status gq_f64(Ctx* ctx, const double* G, int m, const double* Y, cons
   // two column tiles (68 x 2 CTAs at m = 1080), NB = 8-column groups per tile
   const int ct = q > 8 ? 2 : 1;
   const int NB = (q + 8 * ct - 1) / (8 * ct);
-  switch (NB) {
+  static const bool dfma = getenv("TSK_GQ_DFMA") != nullptr;
+  if (!dfma) {
+    switch (NB) {
+      case 1: e = launch_gq3<1>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      case 2: e = launch_gq3<2>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      case 3: e = launch_gq3<3>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      case 4: e = launch_gq3<4>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      case 5: e = launch_gq3<5>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      case 6: e = launch_gq3<6>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      case 7: e = launch_gq3<7>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+      default: e = launch_gq3<8>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    }
+  } else switch (NB) {
     case 1: e = launch_gq2<1>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
     case 2: e = launch_gq2<2>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
     case 3: e = launch_gq2<3>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
@@ -939,6 +1100,7 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       cudaMemcpyAsync(hostbuf, theta, (size_t)pa * 8, cudaMemcpyDeviceToHost, s);
       cudaMemcpyAsync(hostbuf + p, res, (size_t)kr * 8, cudaMemcpyDeviceToHost, s);
       cudaMemcpyAsync(hostbuf + 2 * p, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(hostbuf + 3 * p, Cn, (size_t)pa * 8, cudaMemcpyDeviceToHost, s);  // 1 / L_jj of the CholQR
       return cudaStreamSynchronize(s) == cudaSuccess ? TSK_OK : TSK_ECUDA;
     };
     cudaMemsetAsync(flags, 0, 2 * sizeof(int), s);
@@ -1122,6 +1284,33 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
   }
   copy_cols_kernel<<<nblk((long long)m * kr, 256), 256, 0, s>>>(X, pa, 0, Xo, k, nl, m, kr);
   ctx->count_launch();
+  // The active vectors were projected against the locked ones once per filter (classical Gram-Schmidt):
+  // a second projection of the output (CGS2) removes the eps x amplification left along the locked
+  // directions (a dominant pair over a flat rest: ||S S^T - I|| 1.2e-5 with one pass)
+  if (nl > 0 && kr > 0) {
+    if ((st = gemm_tn_f64(ctx, Xo, k, 0, Xo + nl, k, 0, m, nl, kr, 1, Cl, kr, 0, 0, WS_EIG_SMALL)) != TSK_OK) return st;
+    if ((st = gemm_nn_f64(ctx, Xo, k, 0, Cl, kr, 0, m, nl, kr, 1, nullptr, F0, kr, 0)) != TSK_OK) return st;
+    sub_cols_kernel<<<nblk((long long)m * kr, 256), 256, 0, s>>>(F0, kr, Xo, k, nl, m, kr);
+    ctx->count_launch();
+  }
+  // The Ritz vectors inherit the orthogonality error of the last CholQR basis, ~eps / d_min with d_min the
+  // smallest pivot of the column-scaled block Gram (a deep filter on a dominant-over-flat spectrum reaches
+  // d_min ~ 1e-11, ||S S^T - I|| ~ 1e-5).  Past eps / d_min = 1e-9 the output block gets one more CholQR
+  // pass (same kernels; the Ritz values are unchanged to first order).
+  {
+    double rmax = 0.0;
+    for (int c = 0; c < pa; ++c) rmax = std::max(rmax, hostbuf[3 * p + c]);
+    if (2.220446049250313e-16 * rmax * rmax > 1e-9) {
+      if (trace) fprintf(stderr, "[eig] output re-orthonormalised (eps / d_min = %.1e)\n", 2.22e-16 * rmax * rmax);
+      if ((st = gemm_tn_f64(ctx, Xo, k, 0, Xo, k, 0, m, k, k, 1, M, k, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
+      chol_scale_kernel<<<1, kCiThreads, (size_t)k * (k | 1) * 8, s>>>(M, k, 1e-14, 0.0, Rs, Cn, Cn + p, flags);
+      trsm2_kernel<<<nblk(2LL * m, kTrsmRows), kTrsmRows, ((size_t)k * k + (size_t)kTrsmRows * (k | 1) + 2 * (size_t)k) * 8,
+                     s>>>(Xo, Xo, Cn + p, Rs, Cn, m, k, Y, Z);
+      ctx->count_launch(2);
+      if ((st = launch_status("eig output cholqr")) != TSK_OK) return st;
+      Xo = Y;
+    }
+  }
   write_sketch_kernel<<<k, 256, 0, s>>>(Xo, m, k, S);
   ctx->count_launch();
   if (X64) cudaMemcpyAsync(X64, Xo, (size_t)m * k * 8, cudaMemcpyDeviceToDevice, s);
