@@ -233,16 +233,14 @@ tsk_status cholqr2(Ctx* ctx, const double* Y, double* Q1, double* Q, int m, int 
 // Out[i][c] = alpha * sum_l G[i][l] Y[l][c] + beta * Y[i][c] + gamma * Yp[i][c]   (i < m, c < q)
 // (Y, Yp, Out: [m][ldy]; Yp may be null when gamma == 0): the Chebyshev filter step (the
 // three-term axpy fused into the product epilogue) and the Rayleigh-Ritz product Z = G'Y.
-// CTA (tile, ct) owns rows [16 tile, +16) and columns
-// [BN ct, +BN) of Out over the whole K = m, with G's rows and Y's rows streamed through a cp.async ring
-// of kG2Stages chunks of 32 K (so the L2 latency is paid once per launch, not once per chunk), the 8
-// warps taking interleaved K indices of every chunk (warp w: kk = w, w + 8, ...; lane (rg, cg) owns rows
-// 4 rg + a and columns cg + 8b -- two 16-byte G reads from the transposed chunk and NB conflict-free Y
-// reads feed 4 NB DFMA), and the 8 warp partials summed in fixed order in shared memory before the
-// fused three-term epilogue.
-// 68 x 2 CTAs at m = 1080, no cluster and no global partials: the round-2 split-K kernel (64-row tiles,
-// 8-CTA clusters reducing over DSMEM) spent most of its ~36 us on per-chunk L2 latency, its cluster
-// barriers and the DSMEM reduction (ncu); this one takes ~21 us cold (ncu), C4 top-k 3.5 -> 3.2 ms.
+// CTA (tile, ct) owns rows [16 tile, +16) and columns [BN ct, +BN) of Out over the whole K = m, with G's
+// rows and Y's rows streamed through a cp.async ring of kG2Stages chunks of 32 K (so the L2 latency is paid
+// once per launch, not once per chunk), the products on the fp64 tensor cores (gq3_f64_kernel below), and
+// the 8 warp partials summed in fixed order in shared memory before the fused three-term epilogue.
+// 68 x 2 CTAs at m = 1080, no cluster and no global partials.  Measured (ncu, C4): the round-2 split-K
+// kernel (64-row tiles, 8-CTA clusters reducing over DSMEM) ~36 us, dominated by per-chunk L2 latency,
+// cluster barriers and the DSMEM reduction; this ring with DFMA register tiles ~21-27 us (issue-bound:
+// 2.8 instructions per DFMA); with DMMA ~17 us.
 constexpr int kG2BM = 16, kG2KC = 32, kG2Stages = 6, kG2Threads = 256, kG2Warps = kG2Threads / 32;
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -253,124 +251,9 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
-template <int NB>
-__global__ void __launch_bounds__(kG2Threads) gq2_f64_kernel(const double* __restrict__ G, int m, int ldg,
-                                                             const double* __restrict__ Y,
-                                                             const double* __restrict__ Yp, int q, int ldy,
-                                                             double alpha, double beta, double gamma,
-                                                             double* __restrict__ Out) {
-  constexpr int BN = 8 * NB;
-  constexpr int SG = kG2KC * kG2BM;        // G chunk, transposed: [32 K][16 rows]
-  constexpr int SS = SG + kG2KC * BN;      // + Y chunk [32 K][BN]
-  extern __shared__ __align__(16) double g2_sm[];
-  const int i0 = blockIdx.x * kG2BM, c0 = blockIdx.y * BN;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rg = lane >> 3, cgi = lane & 7;  // rows 4 rg .. 4 rg + 3 (two 16-B reads), columns cgi + 8 b
-  const int nch = (m + kG2KC - 1) / kG2KC;
-  // each thread's copy assignments are the same in every chunk: source pointers (chunk 0), smem
-  // offsets and bounds precomputed once (address arithmetic in the chunk loop made the integer
-  // pipe, not the DFMAs, the limit)
-  constexpr int NGU = (SG + kG2Threads - 1) / kG2Threads;  // 1
-  constexpr int NYU = (kG2KC * BN + kG2Threads - 1) / kG2Threads;
-  const double* gsrc[NGU];
-  int gdst[NGU], gkk[NGU];
-  bool gok[NGU];
-#pragma unroll
-  for (int u = 0; u < NGU; ++u) {
-    const int e = tid + u * kG2Threads, r = e / kG2KC, kk = e % kG2KC;
-    gok[u] = e < SG && i0 + r < m;
-    gsrc[u] = gok[u] ? G + (size_t)(i0 + r) * ldg + kk : G;
-    gdst[u] = kk * kG2BM + r;
-    gkk[u] = kk;
-  }
-  const double* ysrc[NYU];
-  int ykk[NYU];
-  bool yok[NYU];
-#pragma unroll
-  for (int u = 0; u < NYU; ++u) {
-    const int e = tid + u * kG2Threads, kk = e / BN, c = e % BN;
-    yok[u] = e < kG2KC * BN && c0 + c < q;
-    ysrc[u] = yok[u] ? Y + (size_t)kk * ldy + c0 + c : Y;
-    ykk[u] = kk;
-  }
-  auto load = [&](int st, int ch) {
-    double* Gs = g2_sm + st * SS;
-    double* Ys = Gs + SG;
-    const int k0 = ch * kG2KC;
-    const size_t yoff = (size_t)k0 * ldy;
-#pragma unroll
-    for (int u = 0; u < NGU; ++u) {
-      if (tid + u * kG2Threads < SG) {
-        const bool ok = gok[u] && k0 + gkk[u] < m;
-        cp_async8(Gs + gdst[u], ok ? gsrc[u] + k0 : G, ok);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < NYU; ++u) {
-      if (tid + u * kG2Threads < kG2KC * BN) {
-        const bool ok = yok[u] && k0 + ykk[u] < m;
-        cp_async8(Ys + tid + u * kG2Threads, ok ? ysrc[u] + yoff : Y, ok);
-      }
-    }
-  };
-#pragma unroll
-  for (int st = 0; st < kG2Stages - 1; ++st) {
-    if (st < nch) load(st, st);
-    cp_async_commit();
-  }
-  double acc[4][NB];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) acc[a][b] = 0.0;
-  for (int ch = 0; ch < nch; ++ch) {
-    cp_async_wait<kG2Stages - 2>();
-    __syncthreads();  // chunk ch visible to all; every warp is done with the stage refilled below
-    if (ch + kG2Stages - 1 < nch) load((ch + kG2Stages - 1) % kG2Stages, ch + kG2Stages - 1);
-    cp_async_commit();
-    const double* Gs = g2_sm + (ch % kG2Stages) * SS;
-    const double* Ys = Gs + SG;
-#pragma unroll
-    for (int u = 0; u < kG2KC / kG2Warps; ++u) {
-      const int kk = w + kG2Warps * u;
-      const double2 g01 = *reinterpret_cast<const double2*>(Gs + kk * kG2BM + 4 * rg);
-      const double2 g23 = *reinterpret_cast<const double2*>(Gs + kk * kG2BM + 4 * rg + 2);
-      const double av[4] = {g01.x, g01.y, g23.x, g23.y};
-      double bv[NB];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) bv[b] = Ys[kk * BN + cgi + 8 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-    }
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  double* red = g2_sm;  // [8 warps][16][BN] (the ring is free)
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) red[(w * kG2BM + 4 * rg + a) * BN + cgi + 8 * b] = acc[a][b];
-  __syncthreads();
-  for (int e = tid; e < kG2BM * BN; e += kG2Threads) {
-    const int r = e / BN, c = e % BN;
-    const int row = i0 + r, col = c0 + c;
-    if (row >= m || col >= q) continue;
-    double sacc = 0.0;
-#pragma unroll
-    for (int t = 0; t < kG2Warps; ++t) sacc += red[t * kG2BM * BN + e];
-    double v = alpha * sacc;
-    if (beta != 0.0) v = fma(beta, Y[(size_t)row * ldy + col], v);
-    if (gamma != 0.0) v = fma(gamma, Yp[(size_t)row * ldy + col], v);
-    Out[(size_t)row * ldy + col] = v;
-  }
-}
-
-// Tensor-core variant (fp64 mma.sync m8n8k4, DMMA): the same tiles, ring and epilogue; warp w takes the
-// k4-step w of every 32-deep chunk, two 8-row A fragments and NB 8-column B fragments per step feed
-// 2 NB DMMAs (256 FMA each) -- 7 shared loads per 2560 FMA where the DFMA loop above issues 36 loads
-// and 80 DFMAs for the same work.  Shared layouts padded for conflict-free fragment loads (G rows pitch
+// Warp w takes the k4-step w of every 32-deep chunk: two 8-row A fragments and NB 8-column B fragments
+// per step feed 2 NB DMMAs (fp64 mma.sync m8n8k4, 256 FMA each) -- 7 shared loads per 2560 FMA where a
+// DFMA register tile issues 36 loads and 80 DFMAs for the same work.  Shared layouts padded for conflict-free fragment loads (G rows pitch
 // 36, Y rows pitch = BN rounded up to 12 mod 16).
 template <int NB>
 struct Gq3Geom {
@@ -507,22 +390,6 @@ static cudaError_t launch_gq3(int ct, cudaStream_t s, const double* G, int m, co
   return cudaGetLastError();
 }
 
-template <int NB>
-static cudaError_t launch_gq2(int ct, cudaStream_t s, const double* G, int m, const double* Y, const double* Yp, int q,
-                              int ldy, double alpha, double beta, double gamma, double* Out) {
-  constexpr int BN = 8 * NB;
-  const size_t ring = (size_t)kG2Stages * (kG2BM * kG2KC + kG2KC * BN) * sizeof(double);
-  const size_t smem = std::max(ring, (size_t)kG2Warps * kG2BM * BN * sizeof(double));
-  static uint64_t attr = 0;
-  if (!(attr & device_bit())) {
-    cudaFuncSetAttribute(gq2_f64_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr |= device_bit();
-  }
-  gq2_f64_kernel<NB><<<dim3((m + kG2BM - 1) / kG2BM, ct), kG2Threads, smem, s>>>(G, m, m, Y, Yp, q, ldy, alpha, beta,
-                                                                                  gamma, Out);
-  return cudaGetLastError();
-}
-
 // Out = alpha G Y + beta Y + gamma Yp for Y [m][ldy] with q <= 128 columns (fp64)
 static tsk_status gq_f64(Ctx* ctx, const double* G, int m, const double* Y, const double* Yp, int q, int ldy,
                          double alpha, double beta, double gamma, double* Out) {
@@ -532,35 +399,23 @@ static tsk_status gq_f64(Ctx* ctx, const double* G, int m, const double* Y, cons
   // two column tiles (68 x 2 CTAs at m = 1080), NB = 8-column groups per tile
   const int ct = q > 8 ? 2 : 1;
   const int NB = (q + 8 * ct - 1) / (8 * ct);
-  static const bool dfma = getenv("TSK_GQ_DFMA") != nullptr;
-  if (!dfma) {
-    switch (NB) {
-      case 1: e = launch_gq3<1>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 2: e = launch_gq3<2>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 3: e = launch_gq3<3>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 4: e = launch_gq3<4>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 5: e = launch_gq3<5>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 6: e = launch_gq3<6>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      case 7: e = launch_gq3<7>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-      default: e = launch_gq3<8>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    }
-  } else switch (NB) {
-    case 1: e = launch_gq2<1>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    case 2: e = launch_gq2<2>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    case 3: e = launch_gq2<3>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    case 4: e = launch_gq2<4>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    case 5: e = launch_gq2<5>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    case 6: e = launch_gq2<6>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    case 7: e = launch_gq2<7>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
-    default: e = launch_gq2<8>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+  switch (NB) {
+    case 1: e = launch_gq3<1>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 2: e = launch_gq3<2>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 3: e = launch_gq3<3>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 4: e = launch_gq3<4>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 5: e = launch_gq3<5>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 6: e = launch_gq3<6>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    case 7: e = launch_gq3<7>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
+    default: e = launch_gq3<8>(ct, s, G, m, Y, Yp, q, ldy, alpha, beta, gamma, Out); break;
   }
   ctx->count_launch();
   if (e != cudaSuccess) {
-    if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gq2_f64: %s\n", cudaGetErrorString(e));
+    if (getenv("TSK_DEBUG")) fprintf(stderr, "[tsk] gq_f64: %s\n", cudaGetErrorString(e));
     cudaGetLastError();
     return TSK_ECUDA;
   }
-  return launch_status("gq2_f64");
+  return launch_status("gq_f64");
 }
 
 // Out = alpha Z + beta Y + gamma Yp  (elementwise over n; Yp may be null when gamma == 0)
