@@ -556,6 +556,131 @@ __global__ void __launch_bounds__(128) chol_basis_kernel(const double* __restric
   for (int c = tid; c < k; c += nt) mu[(size_t)b * k + c] = c < rk ? 1.0 : 0.0;
 }
 
+// Same contract as chol_basis_kernel for k <= 64 (round 2): pivoted Cholesky of C without row / column
+// swaps (the pivots are chosen among the indices not yet eliminated, the full symmetric matrix is updated in
+// place) and X = L^{-1} accumulated in the same elimination loop, so a step is [warp 0 picks the pivot] |
+// barrier | [all threads: trailing update; the previous step's rank-1 term added to the not-yet-pivoted rows
+// of acc (acc_i = sum_{t<j} L(i, t) X_t); row j of X = (e_j - acc_p) / L_jj, stored in place of acc_p] |
+// barrier -- no serial column solve afterwards (the kernel above: ~6 barriers per step, a mirror pass and
+// one thread per column of L^{-1}; 231 us per 250 C4 matrices).  256 threads.
+constexpr int kCb2Threads = 256, kCb2MaxK = 64;
+__global__ void __launch_bounds__(kCb2Threads) chol_basis2_kernel(const double* __restrict__ Cg, int k,
+                                                                  double* __restrict__ W, double* __restrict__ mu) {
+  extern __shared__ double cb_sm[];
+  const int ld = k + 1;
+  double* A = cb_sm;                 // [k][ld] the symmetric trailing matrix (original indexing)
+  double* AX = cb_sm + (size_t)k * ld;  // [k][ld] acc_i (not yet pivoted i), X row j in row piv[j]
+  __shared__ double ub[2][kCb2MaxK];    // u_j(i) = A(i, p_j) / sqrt(d_j), i not eliminated before step j
+  __shared__ int piv[kCb2MaxK], done[kCb2MaxK];
+  __shared__ double dmax0_s, rs_s;
+  __shared__ int p_s, rank_s;
+  const int b = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const double* Cb = Cg + (size_t)b * k * k;
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, l = e - (e / k) * k;
+    A[i * ld + l] = Cb[e];
+    AX[i * ld + l] = 0.0;
+  }
+  for (int i = tid; i < k; i += nt) {
+    done[i] = 0;
+    ub[0][i] = ub[1][i] = 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double d = 0.0;
+    for (int i = tid; i < k; i += 32) d = fmax(d, A[i * ld + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if (tid == 0) {
+      dmax0_s = d;
+      rank_s = k;
+    }
+  }
+  __syncthreads();
+  const double floor_piv = 1e-13 * dmax0_s;
+  for (int j = 0; j < k; ++j) {
+    if (tid < 32) {  // pivot: largest remaining diagonal (ties -> lowest index)
+      double best = -1.0;
+      int bi = k;
+      for (int i = tid; i < k; i += 32) {
+        const double d = done[i] ? -1.0 : A[i * ld + i];
+        if (d > best) { best = d; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        if (!(best > floor_piv)) {
+          rank_s = j;
+        } else {
+          p_s = bi;
+          piv[j] = bi;
+          done[bi] = 1;
+          rs_s = rsqrt(best);
+        }
+      }
+    }
+    __syncthreads();
+    if (rank_s == j) break;
+    const int p = p_s;
+    const double rs = rs_s;                 // 1 / L_jj
+    const double rd = rs * rs;              // 1 / d_j
+    const double* up = ub[(j - 1) & 1];     // u_{j-1} (zero at j = 0)
+    double* un = ub[j & 1];
+    const double* xprev = j > 0 ? AX + (size_t)piv[j - 1] * ld : nullptr;  // X row j - 1 (pivot order)
+    // u_j and the trailing update of the not-eliminated rows / columns (column p itself is read only);
+    // thread (ty, tx) of the 16 x 16 grid owns rows ty + 16 a and columns tx + 16 b (no index division)
+    const int ty = tid >> 4, tx = tid & 15;
+    if (tid < k) un[tid] = done[tid] ? 0.0 : A[tid * ld + p] * rs;
+    double ci[4], cl[4], ui[4], xc[4];
+    bool di[4], dl[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = ty + 16 * a, l = tx + 16 * a;
+      di[a] = i >= k || done[i];
+      dl[a] = l >= k || done[l];
+      ci[a] = i < k ? A[i * ld + p] * rd : 0.0;
+      cl[a] = l < k ? A[l * ld + p] : 0.0;
+      ui[a] = i < k ? up[i] : 0.0;
+      xc[a] = (j > 0 && l < j) ? xprev[l] : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = ty + 16 * a;
+      if (i >= k) continue;
+      // acc rows: add the step j - 1 term L(i, j-1) X_{j-1} = u_{j-1}(i) X_{j-1} (rows not yet pivoted,
+      // and the new pivot's row p, whose X row j is formed from it after the barrier)
+      const bool acc_row = j > 0 && (!done[i] || i == p);
+#pragma unroll
+      for (int bq = 0; bq < 4; ++bq) {
+        const int l = tx + 16 * bq;
+        if (l >= k) continue;
+        if (!di[a] && !dl[bq]) A[i * ld + l] = fma(-ci[a], cl[bq], A[i * ld + l]);
+        if (acc_row && l < j) AX[i * ld + l] = fma(ui[a], xc[bq], AX[i * ld + l]);
+      }
+    }
+    __syncthreads();
+    // row j of X = L^{-1}: X_jc = (delta_jc - acc_p(c)) / L_jj, c <= j, in place of acc_p
+    for (int c = tid; c <= j; c += nt) AX[p * ld + c] = ((c == j ? 1.0 : 0.0) - (c < j ? AX[p * ld + c] : 0.0)) * rs;
+    __syncthreads();
+  }
+  const int rk = rank_s;
+  double* Wb = W + (size_t)b * k * k;
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, c = e - (e / k) * k;  // W[piv[i]][c] = Linv[c][i] = X row c (in row piv[c]), column i
+    if (i < rk) Wb[(size_t)piv[i] * k + c] = (c < rk && i <= c) ? AX[(size_t)piv[c] * ld + i] : 0.0;
+  }
+  // indices never pivoted (rank < k): zero rows of W (done[] marks exactly the pivoted indices)
+  for (int e = tid; e < k * k; e += nt) {
+    const int a = e / k;
+    if (!done[a]) Wb[e] = 0.0;
+  }
+  for (int c = tid; c < k; c += nt) mu[(size_t)b * k + c] = c < rk ? 1.0 : 0.0;
+}
+
 // below err^2 = tau ||A||^2 the Pythagorean error is replaced by the dense residual (reading c17)
 constexpr double kScwPythTau = 3e-3;
 
@@ -603,6 +728,8 @@ static void scw_attrs() {
     cudaFuncSetAttribute(scw_combine_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
+    cudaFuncSetAttribute(chol_basis2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         2 * kCb2MaxK * (kCb2MaxK + 1) * 8);
     attr |= device_bit();
   }
 }
@@ -711,7 +838,10 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     ctx->count_launch(1);
     if ((st = launch_status("scw gram(SA)")) != TSK_OK) return st;
     if ((size_t)2 * k * (k + 1) * 8 <= (size_t)kCholSmemMax) {
-      chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cb, k, Wc, mu);
+      if (k <= kCb2MaxK && !getenv("TSK_SCW_CHOL1"))
+        chol_basis2_kernel<<<bc, kCb2Threads, (size_t)2 * k * (k + 1) * 8, s>>>(Cb, k, Wc, mu);
+      else
+        chol_basis_kernel<<<bc, 128, (size_t)2 * k * (k + 1) * 8, s>>>(Cb, k, Wc, mu);
       ctx->count_launch(1);
       if ((st = launch_status("scw chol_basis")) != TSK_OK) return st;
     } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10, nullptr, eigws)) != TSK_OK) {
