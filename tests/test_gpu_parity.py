@@ -138,9 +138,12 @@ def _check_sketch(S, lam, G_o, lam_o, k, projector, G_gpu=None):
     if G_gpu is not None:  # eigensolver accuracy on its own input
         lam_g = np.sort(np.linalg.eigvalsh(G_gpu))[::-1]
         assert abs(kyfan_deficit(G_gpu, lam_g, Sg)) <= KYFAN_SOLVER_TOL
-        # Ritz values come from the 3xTF32 G Q product, whose truncating TMEM accumulation biases
-        # the dominant direction by ~1e-6 (measured 1.04e-6 at C4): bound 2e-6 theta_1
-        assert np.all(np.abs(lg - lam_g[:k]) <= 2e-6 * lam_g[0])
+        # Rayleigh-Ritz values are lower bounds of the top eigenvalues (Cauchy interlacing, theta_i <= lambda_i,
+        # up to fp64 rounding: the G'Y products are fp64 for m <= 2048) and their total shortfall is the Ky Fan
+        # deficit the solver stops on (reading c15), so each lies within that deficit of its eigenvalue
+        short = lam_g[:k] - lg
+        assert np.all(short >= -1e-12 * lam_g[0])
+        assert np.all(short <= KYFAN_SOLVER_TOL * lam_g[:k].sum() + 1e-12 * lam_g[0])
     if projector:
         S_o, _ = tucker1.top_k_eigen(G_o, k)
         assert tucker1.eigengap(lam_o, k) >= 1.05
