@@ -387,7 +387,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128 KB through shared memory (TMA 32 + transform 48 + MMA-B 48) instead of 192 KB.
 // TMEM: two 128-column accumulators (double buffer; H H^T and the cross terms share one) + three
 // 64-column A stages [H_X | L_X].  Shared memory: 5 raw TMA stages [X|Y] + 3 lo stages [L_Y].
-constexpr int kTsLoStages = 3;
+// transform -> MMA ring depth (TMEM A stages [H_X | L_X] and smem lo stages): 4 (TMEM 2 x 128 + 4 x 64 = 512
+// columns) unless the lo stages are [H_Y | L_Y] (kYT: 32 KB each, 3 fit shared memory)
+template <bool kN64, bool kYT>
+constexpr int ts_lo_stages() { return kYT ? 3 : 4; }
 // Split rounding (TS kernel): hi(x) = x rounded to nearest tf32 for the X operand (written to TMEM), and
 // lo = x - hi, which then has a random sign: the tensor core truncates its operands, so truncated hi
 // parts leave lo with the sign of x and the dropped lo x lo' and the truncation of lo bias every product
@@ -405,7 +408,8 @@ template <bool kN64, bool kYT>
 constexpr int ts_lo_stage_bytes() { return kYT ? 2 * kTileBytes : (kN64 ? kTileBytes / 2 : kTileBytes); }
 template <bool kN64, bool kYT>
 constexpr int ts_smem_bytes() {
-  return ts_raw_stages<kN64, kYT>() * ts_raw_stage_bytes<kN64, kYT>() + kTsLoStages * ts_lo_stage_bytes<kN64, kYT>() +
+  return ts_raw_stages<kN64, kYT>() * ts_raw_stage_bytes<kN64, kYT>() +
+         ts_lo_stages<kN64, kYT>() * ts_lo_stage_bytes<kN64, kYT>() +
          1024 + 256;
 }
 constexpr int kTsSmemBytes = ts_smem_bytes<false, false>();
@@ -423,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int RS = ts_raw_stages<kN64, kYT>();          // raw ring depth
   constexpr int RSB = ts_raw_stage_bytes<kN64, kYT>();    // raw stage: [X | Y] (Y = bn x 32 fp32)
   constexpr int LB = ts_lo_stage_bytes<kN64, kYT>();      // lo stage: [L_Y] or [H_Y | L_Y]
+  constexpr int kTsLoStages = ts_lo_stages<kN64, kYT>();
   // N = 64 (SCW's SA / AV products): the split transform is the critical path (one warp per SM
   // sub-partition, latency-bound), so warps 12-15 join it -- two warps per TMEM lane quadrant, each
   // converting 16 of the chunk's 32 K-columns -- and the 64-column epilogue runs on warps 8-11
