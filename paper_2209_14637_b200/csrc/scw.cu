@@ -185,6 +185,83 @@ static void launch_combine2(const float* In, const double* W, const double* mu, 
         In, W, mu, k, len, nout, ldw, wst, Out, ldo, only);
 }
 
+// V^T = sc (W^T B) for k <= 64 on the fp64 tensor cores (round 2): V^T[c][j] = sc_c sum_a W[a][c] B[a][j], one CTA
+// per (matrix, 128 columns j), 4 warps; W^T is staged once per CTA (rows c, pitch 68: conflict-free A
+// fragments), B streamed 32 columns at a time as fp64 (pitch 44: conflict-free B fragments); warp w owns
+// the output rows 16 w .. 16 w + 15 (two m8 tiles) x the 4 n8 tiles of a 32-column block, 2 x 4 DMMA
+// (mma.sync m8n8k4 f64) per k4 step.  The DFMA tile kernel above reached ~33 % of the fp64 rate here
+// (287 us per 250 C4 matrices).
+constexpr int kVtCols = 128, kVtBlk = 32, kVtWP = 68, kVtBP = 44;
+constexpr size_t kVtSmem = (size_t)64 * (kVtWP + kVtBP) * sizeof(double);
+__global__ void __launch_bounds__(128) scw_vt_dmma_kernel(const float* __restrict__ In, const double* __restrict__ W,
+                                                          const double* __restrict__ mu, int k, int len, long long wst,
+                                                          float* __restrict__ Out) {
+  extern __shared__ __align__(16) double vt_sm[];
+  double (*Wt)[kVtWP] = reinterpret_cast<double (*)[kVtWP]>(vt_sm);             // [64][kVtWP]
+  double (*Bs)[kVtBP] = reinterpret_cast<double (*)[kVtBP]>(vt_sm + 64 * kVtWP);  // [64][kVtBP]
+  __shared__ double sc[64];
+  const int b = blockIdx.y, jbase = blockIdx.x * kVtCols;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const double* Wb = W + (size_t)b * wst;
+  const float* Ib = In + (size_t)b * k * len;
+  float* Ob = Out + (size_t)b * k * len;
+  const int kp = (k + 3) & ~3;  // K padded to the k4 step (zero rows / columns)
+  for (int e = tid; e < 64 * 64; e += 128) {
+    const int c = e >> 6, a = e & 63;  // Wt[c][a] = W[a][c]
+    Wt[c][a] = (c < k && a < k) ? Wb[(size_t)a * k + c] : 0.0;
+  }
+  for (int c = tid; c < 64; c += 128) {
+    double v = 0.0;
+    if (c < k) {
+      const double m0 = mu[(size_t)b * k], mc = mu[(size_t)b * k + c];
+      v = (mc > 0.0 && mc > 1e-13 * m0) ? 1.0 / sqrt(mc) : 0.0;
+    }
+    sc[c] = v;
+  }
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int j0 = jbase; j0 < min(jbase + kVtCols, len); j0 += kVtBlk) {
+    __syncthreads();  // Wt / sc staged; the previous block's Bs consumed
+    for (int e = tid; e < 64 * kVtBlk; e += 128) {
+      const int a = e >> 5, jj = e & 31;
+      Bs[a][jj] = (a < k && j0 + jj < len) ? (double)Ib[(size_t)a * len + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+    double acc[2][4][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const int r0 = 16 * w;
+    for (int a0 = 0; a0 < kp; a0 += 4) {
+      const double x0 = Wt[r0 + fr][a0 + fk], x1 = Wt[r0 + 8 + fr][a0 + fk];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const double y = Bs[a0 + fk][8 * nt + fr];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[0][nt][0]), "+d"(acc[0][nt][1]) : "d"(x0), "d"(y));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[1][nt][0]), "+d"(acc[1][nt][1]) : "d"(x1), "d"(y));
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int c = r0 + 8 * mt + fr;
+      if (c >= k) continue;
+      const double scl = sc[c];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int j = j0 + 8 * nt + 2 * fk;
+        if (j + 1 < len) {
+          *reinterpret_cast<float2*>(Ob + (size_t)c * len + j) =
+              make_float2((float)(acc[mt][nt][0] * scl), (float)(acc[mt][nt][1] * scl));
+        } else if (j < len) {
+          Ob[(size_t)c * len + j] = (float)(acc[mt][nt][0] * scl);
+        }
+      }
+    }
+  }
+}
+
 static inline size_t combine_smem(int k, int nout) {
   return ((size_t)k * ((nout + 1) & ~1) + 16 + nout) * sizeof(double);
 }
@@ -728,6 +805,7 @@ static void scw_attrs() {
     cudaFuncSetAttribute(scw_combine_kernel<64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(scw_combine_kernel<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(chol_basis_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCholSmemMax);
+    cudaFuncSetAttribute(scw_vt_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kVtSmem);
     cudaFuncSetAttribute(chol_basis2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          2 * kCb2MaxK * (kCb2MaxK + 1) * 8);
     attr |= device_bit();
@@ -847,7 +925,10 @@ tsk_status scw_run(Ctx* ctx, const float* A, long long B, int m, int n, const fl
     } else if ((st = jacobi_eig_batched(ctx, Cb, k, bc, Wc, mu, nullptr, 1e-10, nullptr, eigws)) != TSK_OK) {
       return st;
     }
-    launch_combine2<true>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0, bc, s);
+    if (k <= 64 && (n & 1) == 0 && !getenv("TSK_SCW_VT_DFMA"))
+      scw_vt_dmma_kernel<<<dim3((n + kVtCols - 1) / kVtCols, bc), 128, kVtSmem, s>>>(Bm, Wc, mu, k, n, (long long)kk, Vt);
+    else
+      launch_combine2<true>(Bm, Wc, mu, k, n, k, k, (long long)kk, Vt, 0, bc, s);
     ctx->count_launch();
     if ((st = launch_status("scw vt")) != TSK_OK) return st;
     // 3. Z^T = V^T A^T
