@@ -478,9 +478,104 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGsThreads, 4)
   cluster_sync();  // CTA 1's partial stays readable until CTA 0 is done
 }
 
+// The same Gram on the fp64 tensor cores (DMMA m8n8k4, round 2): the 36 lower-triangle 8 x 8 tiles of the padded
+// 64 x 64 result, 4 warps owning the tile rows {7, 0}, {6, 1}, {5, 2}, {4, 3} (9 tiles each); per k4 step a warp
+// loads the <= 8 fragments v_t = X[8t .. 8t + 7][k .. k + 3] it needs (the A fragment of tile row t and the B
+// fragment of tile column t are the same 8-byte pattern of the transposed chunk, pitch 68: conflict-free) and
+// issues 9 DMMAs -- against 16 DFMA per 4 16-byte loads per thread for the register tiles above.  Same
+// 2-CTA cluster split of len and DSMEM reduction.
+constexpr int kGdThreads = 128, kGdKC = 32, kGdP = 68;
+template <int MA>
+__device__ __forceinline__ void gd_chunk(const double (*xs)[68], int fk, int fr, double (&acc)[9][2]) {
+  constexpr int MB = 7 - MA;
+#pragma unroll 2
+  for (int k4 = 0; k4 < 32; k4 += 4) {
+    double v[MA + 1];
+#pragma unroll
+    for (int t = 0; t <= MA; ++t) v[t] = xs[k4 + fk][8 * t + fr];
+#pragma unroll
+    for (int t = 0; t <= MA; ++t)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[t][0]), "+d"(acc[t][1]) : "d"(v[MA]), "d"(v[t]));
+#pragma unroll
+    for (int t = 0; t <= MB; ++t)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[MA + 1 + t][0]), "+d"(acc[MA + 1 + t][1]) : "d"(v[MB]), "d"(v[t]));
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGdThreads)
+    gram_rows_dmma_kernel(const float* __restrict__ X, int k, int len, double* __restrict__ C) {
+  __shared__ __align__(16) double xs[kGdKC][kGdP];
+  __shared__ __align__(16) double part[4][9][2][32];
+  const int b = blockIdx.x >> 1;
+  const unsigned rank = cluster_ctarank();
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int mA = 7 - w, mB = w;  // tile rows of this warp: mA + 1 + mB + 1 = 9 tiles
+  const int half = ((len + 2 * kGdKC - 1) / (2 * kGdKC)) * kGdKC;
+  const int j0 = rank == 0 ? 0 : half, j1 = rank == 0 ? min(half, len) : len;
+  const float* Xb = X + (size_t)b * k * len;
+  double acc[9][2];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) acc[t][0] = acc[t][1] = 0.0;
+  constexpr int kItems = 16 * kGdKC, kPer = kItems / kGdThreads;  // (column, 4-row group) items, 4 per thread
+  for (int jc = j0; jc < j1; jc += kGdKC) {
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int e = tid + t * kGdThreads, kk = e & 31, g = e >> 5;
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = 4 * g + u;
+        v[u] = (r < k && jc + kk < j1) ? __ldg(Xb + (size_t)r * len + jc + kk) : 0.0f;
+      }
+      *reinterpret_cast<double2*>(&xs[kk][4 * g]) = make_double2((double)v[0], (double)v[1]);
+      *reinterpret_cast<double2*>(&xs[kk][4 * g + 2]) = make_double2((double)v[2], (double)v[3]);
+    }
+    __syncthreads();
+    switch (w) {  // compile-time tile rows per warp (register-resident fragments and accumulators)
+      case 0: gd_chunk<7>(xs, fk, fr, acc); break;
+      case 1: gd_chunk<6>(xs, fk, fr, acc); break;
+      case 2: gd_chunk<5>(xs, fk, fr, acc); break;
+      default: gd_chunk<4>(xs, fk, fr, acc); break;
+    }
+  }
+  if (rank == 1) {
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      part[w][t][0][lane] = acc[t][0];
+      part[w][t][1][lane] = acc[t][1];
+    }
+  }
+  cluster_sync();
+  if (rank == 0) {
+    double* Cb = C + (size_t)b * k * k;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {  // tile q: (mA, q) for q <= mA, else (mB, q - mA - 1)
+      const int mi = q <= mA ? mA : mB, t = q <= mA ? q : q - mA - 1;
+      const int i = 8 * mi + fr;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jj = 8 * t + 2 * fk + h;
+        const double val = acc[q][h] + ld_dsmem_f64(mapa_shared(smem_u32(&part[w][q][h][lane]), 1));
+        if (i < k && jj < k && jj <= i) {
+          Cb[(size_t)i * k + jj] = val;
+          Cb[(size_t)jj * k + i] = val;
+        }
+      }
+    }
+  }
+  cluster_sync();
+}
+
 static void launch_gram_rows_tiled(const float* X, int k, int len, int batch, double* C, cudaStream_t s) {
   if (k <= 64 && batch > 0) {
-    gram_rows_sym_kernel<<<2 * batch, kGsThreads, 0, s>>>(X, k, len, C);
+    if (getenv("TSK_SCW_GRAM_DFMA"))
+      gram_rows_sym_kernel<<<2 * batch, kGsThreads, 0, s>>>(X, k, len, C);
+    else
+      gram_rows_dmma_kernel<<<2 * batch, kGdThreads, 0, s>>>(X, k, len, C);
     return;
   }
   const int nt = (k + 63) / 64;
