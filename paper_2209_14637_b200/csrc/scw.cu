@@ -219,19 +219,34 @@ __global__ void __launch_bounds__(128) scw_vt_dmma_kernel(const float* __restric
     sc[c] = v;
   }
   const int fr = lane >> 2, fk = lane & 3;
-  for (int j0 = jbase; j0 < min(jbase + kVtCols, len); j0 += kVtBlk) {
+  // the next 32-column block of B is loaded into registers while the current one is multiplied
+  constexpr int kPre = 64 * kVtBlk / 128;  // 16 floats per thread
+  float pre[kPre];
+  auto fetch = [&](int j0) {
+#pragma unroll
+    for (int t = 0; t < kPre; ++t) {
+      const int e = tid + t * 128, a = e >> 5, jj = e & 31;
+      pre[t] = (a < k && j0 + jj < len) ? __ldg(Ib + (size_t)a * len + j0 + jj) : 0.0f;
+    }
+  };
+  const int jend = min(jbase + kVtCols, len);
+  fetch(jbase);
+  for (int j0 = jbase; j0 < jend; j0 += kVtBlk) {
     __syncthreads();  // Wt / sc staged; the previous block's Bs consumed
-    for (int e = tid; e < 64 * kVtBlk; e += 128) {
-      const int a = e >> 5, jj = e & 31;
-      Bs[a][jj] = (a < k && j0 + jj < len) ? (double)Ib[(size_t)a * len + j0 + jj] : 0.0;
+#pragma unroll
+    for (int t = 0; t < kPre; ++t) {
+      const int e = tid + t * 128;
+      Bs[e >> 5][e & 31] = (double)pre[t];
     }
     __syncthreads();
+    if (j0 + kVtBlk < jend) fetch(j0 + kVtBlk);
     double acc[2][4][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
     const int r0 = 16 * w;
+#pragma unroll 4
     for (int a0 = 0; a0 < kp; a0 += 4) {
       const double x0 = Wt[r0 + fr][a0 + fk], x1 = Wt[r0 + 8 + fr][a0 + fk];
 #pragma unroll
