@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kCiThreads) chol_scale_kernel(const double* __
       if (tid == 0 && fail == 0) fail = j + 1;
       d = 1.0;
     }
-    const double inv_d = __drcp_rn(d);
+    const double inv_d = fast_rcp(d);
     for (int i = j + 1 + ty; i < p; i += 32) {
       const double f = A[i * ld + j] * inv_d;
       double* row = A + i * ld;

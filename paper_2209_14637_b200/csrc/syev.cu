@@ -343,8 +343,8 @@ __global__ void __launch_bounds__(kTrdThreads) trd_reg_kernel(const double* __re
     if (s2 > 0.0) {
       const double mu = sqrt(fma(alpha, alpha, s2));
       beta = alpha <= 0.0 ? mu : -mu;
-      tau = (beta - alpha) * __drcp_rn(beta);
-      scal = __drcp_rn(alpha - beta);
+      tau = (beta - alpha) * fast_rcp(beta);
+      scal = fast_rcp(alpha - beta);
     }
     auto vval = [&](int i) -> double {  // v_j at absolute index i (0 for i <= j)
       return i == j + 1 ? 1.0 : (i > j + 1 && i < p ? xcol(i) * scal : 0.0);
@@ -505,8 +505,8 @@ __global__ void __launch_bounds__(256) trd_warp_kernel(const double* __restrict_
     if (s2 > 0.0) {
       const double mu = sqrt(fma(alpha, alpha, s2));
       beta = alpha <= 0.0 ? mu : -mu;
-      tau = (beta - alpha) * __drcp_rn(beta);
-      scal = __drcp_rn(alpha - beta);
+      tau = (beta - alpha) * fast_rcp(beta);
+      scal = fast_rcp(alpha - beta);
     }
     for (int i = j + 1 + lane; i < p; i += 32) {
       const double vi = i == j + 1 ? 1.0 : A[i * ld + j] * scal;
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(kTevThreads) tev_kernel(const double* __restri
     Dp[0] = D;
     for (int k = 0; k + 1 < p; ++k) {
       if (fabs(D) < pivmin) D = -pivmin;
-      const double L = e[k] * __drcp_rn(D);
+      const double L = e[k] * fast_rcp(D);
       Lp[k] = L;
       D = (d[k + 1] - lm) - L * e[k];
       Dp[k + 1] = D;
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(kTevThreads) tev_kernel(const double* __restri
     Dm[p - 1] = D;
     for (int k = p - 1; k > 0; --k) {
       if (fabs(D) < pivmin) D = -pivmin;
-      const double U = e[k - 1] * __drcp_rn(D);
+      const double U = e[k - 1] * fast_rcp(D);
       Um[k - 1] = U;
       D = (d[k - 1] - lm) - U * e[k - 1];
       Dm[k - 1] = D;
@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(1024) tev_cta_kernel(const double* __restrict_
       Dp[0] = D;
       for (int k = 0; k + 1 < p; ++k) {
         if (fabs(D) < pivmin) D = -pivmin;
-        const double L = e[k] * __drcp_rn(D);
+        const double L = e[k] * fast_rcp(D);
         Lp[k] = L;
         D = (d[k + 1] - lm) - L * e[k];
         Dp[k + 1] = D;
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(1024) tev_cta_kernel(const double* __restrict_
       Dm[p - 1] = D;
       for (int k = p - 1; k > 0; --k) {
         if (fabs(D) < pivmin) D = -pivmin;
-        const double U = e[k - 1] * __drcp_rn(D);
+        const double U = e[k - 1] * fast_rcp(D);
         Um[k - 1] = U;
         D = (d[k - 1] - lm) - U * e[k - 1];
         Dm[k - 1] = D;

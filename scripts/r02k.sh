@@ -1,4 +1,6 @@
+timeout 200 python scripts/eig_bench.py C4 C3 C5 2>&1 | grep topk | awk 'NR%3==0'
+PROFILE=1 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/eigl.csv python scripts/eig_bench.py C4 > /dev/null 2>&1
+python scripts/launch_summary.py gpurun_out/eigl.csv > gpurun_out/eigl.txt 2>/dev/null; head -6 gpurun_out/eigl.txt
 timeout 200 python scripts/scw_prof.py C4 2>&1 | grep scw_error
-timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/scwl.csv python scripts/scw_prof.py C4 > /dev/null 2>&1
-python scripts/launch_summary.py gpurun_out/scwl.csv > gpurun_out/scwl.txt 2>/dev/null; head -8 gpurun_out/scwl.txt
-timeout 900 python -m pytest tests -m gpu -x -q -k "scw or SCW or end_to_end or parity or c5 or full" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_random_shapes.py tests/test_gpu_full_size.py -x -q 2>&1 | tail -1
+timeout 300 python scripts/random_sweep.py spectra 40 43 2>&1 | tail -1
