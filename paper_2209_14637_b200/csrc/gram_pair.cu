@@ -313,16 +313,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t src = smem_u32(y_ptr(rs)) + (uint32_t)zs * ysub;
             const uint32_t dst = smem_u32(l_ptr(ls));
             const int g = xw ? tt : 128 + tt;
-#pragma unroll 2
-            for (int i = g; i < ychunks; i += 192) {
-              const uint32_t off = (uint32_t)i * 16u;
-              const float4 v = lds_f4(src + off);
-              float4 l;
-              l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-              l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-              l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-              l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-              sts_f4(dst + off, l);
+            // <= 3 float4 per thread (ychunks <= 512): all loads issued before the first use, so one shared-
+            // memory latency is paid per chunk instead of one per item (the compiler reused one register
+            // quadruple for a rolled loop and serialised load -> split -> store)
+            float4 v[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+              if (g + 192 * q < ychunks) v[q] = lds_f4(src + (uint32_t)(g + 192 * q) * 16u);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              if (g + 192 * q < ychunks) {
+                float4 l;
+                l.x = v[q].x - __uint_as_float(__float_as_uint(v[q].x) & 0xFFFFE000u);
+                l.y = v[q].y - __uint_as_float(__float_as_uint(v[q].y) & 0xFFFFE000u);
+                l.z = v[q].z - __uint_as_float(__float_as_uint(v[q].z) & 0xFFFFE000u);
+                l.w = v[q].w - __uint_as_float(__float_as_uint(v[q].w) & 0xFFFFE000u);
+                sts_f4(dst + (uint32_t)(g + 192 * q) * 16u, l);
+              }
             }
             if (xw) tmem_st_wait();
           }

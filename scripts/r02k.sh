@@ -1,6 +1,3 @@
-timeout 200 python scripts/eig_bench.py C4 C3 C5 2>&1 | grep topk | awk 'NR%3==0'
-PROFILE=1 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/eigl.csv python scripts/eig_bench.py C4 > /dev/null 2>&1
-python scripts/launch_summary.py gpurun_out/eigl.csv > gpurun_out/eigl.txt 2>/dev/null; head -6 gpurun_out/eigl.txt
-timeout 200 python scripts/scw_prof.py C4 2>&1 | grep scw_error
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_random_shapes.py tests/test_gpu_full_size.py -x -q 2>&1 | tail -1
-timeout 300 python scripts/random_sweep.py spectra 40 43 2>&1 | tail -1
+python scripts/gram_pair_time.py 1080,1920,2000 "0:4:0:,0:4:0:,0:4:0:" 2>&1 | grep mode
+timeout 300 python scripts/gram_fold.py C4 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_size.py tests/test_gpu_streaming.py -x -q 2>&1 | tail -1
