@@ -568,48 +568,67 @@ __global__ void __launch_bounds__(kCiThreads) chol_scale_kernel(const double* __
   if (tid == 0 && fail) flag[0] = fail;
 }
 
-// Q = (Y diag(s)) L^{-T} and GQ = (Z diag(s)) L^{-T}: row-parallel forward substitution
-// q L^T = y (q_c = (y_c s_c - sum_{a<c} q_a L_ca) / L_cc), one thread per row of Y or Z (rows
-// [0, m) of Y then [m, 2m) of Z), L and the thread's q row in shared memory.
-constexpr int kTrsmRows = 64;
-__global__ void __launch_bounds__(kTrsmRows) trsm2_kernel(const double* __restrict__ Y, const double* __restrict__ Z,
-                                                          const double* __restrict__ s, const double* __restrict__ L,
-                                                          const double* __restrict__ rinv, int m, int p,
-                                                          double* __restrict__ Q, double* __restrict__ GQ) {
-  extern __shared__ double tr_sm[];
-  const int ldq = p | 1;
-  double* Ls = tr_sm;                          // [p][p]
-  double* qs = tr_sm + (size_t)p * p;          // [kTrsmRows][ldq]
-  double* ss = qs + (size_t)kTrsmRows * ldq;   // [p] s
-  double* rs = ss + p;                         // [p] 1 / L_cc
+// Q = (Y diag(s)) L^{-T} and GQ = (Z diag(s)) L^{-T} (rows [0, m) of Y, then [m, 2m) of Z), a warp per row
+// (round 2): the substitution q_c = (y_c s_c - sum_{a<c} q_a L_ca) / L_cc runs over c with the dot product split across the lanes (lane l holds q_a for a = l + 32 j) and a
+// butterfly sum per step -- ~160 cycles per step against a thread-serial chain of c FMAs with its shared-
+// memory loads (the round-2 thread-per-row kernel: 34 CTAs of 64 threads at m = 1080, 40 us; this 22 us).
+// 8 rows per CTA, L / s / 1/L_cc staged in shared memory; p <= 128.
+constexpr int kTwRows = 8;
+__global__ void __launch_bounds__(32 * kTwRows) trsm_warp_kernel(const double* __restrict__ Y,
+                                                                  const double* __restrict__ Z,
+                                                                  const double* __restrict__ s,
+                                                                  const double* __restrict__ L,
+                                                                  const double* __restrict__ rinv, int m, int p,
+                                                                  double* __restrict__ Q, double* __restrict__ GQ) {
+  extern __shared__ double tw_sm[];
+  double* Ls = tw_sm;                  // [p][p]
+  double* ss = tw_sm + (size_t)p * p;  // [p]
+  double* rs = ss + p;                 // [p]
   copy_to_shared_f64(Ls, L, p * p, threadIdx.x, blockDim.x);
   for (int c = threadIdx.x; c < p; c += blockDim.x) {
     ss[c] = s[c];
     rs[c] = rinv[c];
   }
   __syncthreads();
-  const int row = blockIdx.x * kTrsmRows + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kTwRows + (threadIdx.x >> 5);
   if (row >= 2 * m) return;
   const double* y = row < m ? Y + (size_t)row * p : Z + (size_t)(row - m) * p;
   double* out = row < m ? Q + (size_t)row * p : GQ + (size_t)(row - m) * p;
-  double* q = qs + (size_t)threadIdx.x * ldq;
-#pragma unroll 8
-  for (int c = 0; c < p; ++c) q[c] = __ldg(y + c) * ss[c];  // independent loads, one latency
+  double yv[4], q[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int a = lane + 32 * j;
+    yv[j] = a < p ? __ldg(y + a) * ss[a] : 0.0;
+    q[j] = 0.0;
+  }
   for (int c = 0; c < p; ++c) {
     const double* Lc = Ls + (size_t)c * p;
-    double a0 = q[c], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int a = 0;
-    for (; a + 3 < c; a += 4) {
-      a0 = fma(-q[a], Lc[a], a0);
-      a1 = fma(-q[a + 1], Lc[a + 1], a1);
-      a2 = fma(-q[a + 2], Lc[a + 2], a2);
-      a3 = fma(-q[a + 3], Lc[a + 3], a3);
+    double part = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = lane + 32 * j;
+      if (a < c) part = fma(q[j], Lc[a], part);
     }
-    for (; a < c; ++a) a0 = fma(-q[a], Lc[a], a0);
-    q[c] = ((a0 + a1) + (a2 + a3)) * rs[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const int jc = c >> 5, lc = c & 31;
+    const double ysel = jc == 0 ? yv[0] : jc == 1 ? yv[1] : jc == 2 ? yv[2] : yv[3];
+    const double yc = __shfl_sync(0xffffffffu, ysel, lc);
+    const double qc = (yc - part) * rs[c];
+    if (lane == lc) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j == jc) q[j] = qc;
+    }
   }
-  for (int c = 0; c < p; ++c) out[c] = q[c];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int a = lane + 32 * j;
+    if (a < p) out[a] = q[j];
+  }
 }
+static inline size_t trsm_warp_smem(int p) { return ((size_t)p * p + 2 * (size_t)p) * sizeof(double); }
 
 // ---------------------------------------------------------------- Householder QR (fallback)
 // Q = first p columns of the orthogonal factor of Y (m x p, row-major, in place), by Householder
@@ -903,7 +922,7 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
   static uint64_t attr = 0;
   if (!(attr & device_bit())) {
     cudaFuncSetAttribute(chol_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(trsm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(trsm_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_warp_smem(128));
     attr |= device_bit();
   }
 
@@ -932,9 +951,8 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       tsk_status r;
       if ((r = gemm_tn_f64(ctx, Yin, pa, 0, Yin, pa, 0, m, pa, pa, 1, M, pa, 0, 1, WS_EIG_SMALL)) != TSK_OK) return r;
       chol_scale_kernel<<<1, kCiThreads, (size_t)pa * (pa | 1) * 8, s>>>(M, pa, 1e-14, shift, Rs, Cn, Cn + p, flags);
-      trsm2_kernel<<<nblk(2LL * m, kTrsmRows), kTrsmRows,
-                     ((size_t)pa * pa + (size_t)kTrsmRows * (pa | 1) + 2 * (size_t)pa) * 8, s>>>(Yin, Zin, Cn + p, Rs,
-                                                                                             Cn, m, pa, Yout, Zout);
+      trsm_warp_kernel<<<nblk(2LL * m, kTwRows), 32 * kTwRows, trsm_warp_smem(pa), s>>>(Yin, Zin, Cn + p, Rs, Cn, m,
+                                                                                         pa, Yout, Zout);
       ctx->count_launch(2);
       return launch_status("eig cholqr");
     };
@@ -979,9 +997,8 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       if (st != TSK_OK) return st;
       if ((st = product(Y, nullptr, pa, 1.0, 0.0, 0.0, Z)) != TSK_OK) return st;
       cudaStreamWaitEvent(s, ctx->ev[1], 0);
-      trsm2_kernel<<<nblk(2LL * m, kTrsmRows), kTrsmRows,
-                     ((size_t)pa * pa + (size_t)kTrsmRows * (pa | 1) + 2 * (size_t)pa) * 8, s>>>(Y, Z, Cn + p, Rs, Cn,
-                                                                                             m, pa, Q, GQ);
+      trsm_warp_kernel<<<nblk(2LL * m, kTwRows), 32 * kTwRows, trsm_warp_smem(pa), s>>>(Y, Z, Cn + p, Rs, Cn, m, pa,
+                                                                                         Q, GQ);
       ctx->count_launch();
       if ((st = launch_status("eig cholqr")) != TSK_OK) return st;
     }
@@ -1159,8 +1176,8 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       if (trace) fprintf(stderr, "[eig] output re-orthonormalised (eps / d_min = %.1e)\n", 2.22e-16 * rmax * rmax);
       if ((st = gemm_tn_f64(ctx, Xo, k, 0, Xo, k, 0, m, k, k, 1, M, k, 0, 1, WS_EIG_SMALL)) != TSK_OK) return st;
       chol_scale_kernel<<<1, kCiThreads, (size_t)k * (k | 1) * 8, s>>>(M, k, 1e-14, 0.0, Rs, Cn, Cn + p, flags);
-      trsm2_kernel<<<nblk(2LL * m, kTrsmRows), kTrsmRows, ((size_t)k * k + (size_t)kTrsmRows * (k | 1) + 2 * (size_t)k) * 8,
-                     s>>>(Xo, Xo, Cn + p, Rs, Cn, m, k, Y, Z);
+      trsm_warp_kernel<<<nblk(2LL * m, kTwRows), 32 * kTwRows, trsm_warp_smem(k), s>>>(Xo, Xo, Cn + p, Rs, Cn, m, k, Y,
+                                                                                        Z);
       ctx->count_launch(2);
       if ((st = launch_status("eig output cholqr")) != TSK_OK) return st;
       Xo = Y;

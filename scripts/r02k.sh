@@ -1,3 +1,5 @@
-python scripts/gram_pair_time.py 1080,1920,2000 "0:4:0:,0:4:0:,0:4:0:" 2>&1 | grep mode
-timeout 300 python scripts/gram_fold.py C4 2>&1 | tail -1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_size.py tests/test_gpu_streaming.py -x -q 2>&1 | tail -1
+timeout 200 python scripts/eig_bench.py C4 C3 C5 2>&1 | grep topk | awk 'NR%3==0'
+PROFILE=1 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/eigl.csv python scripts/eig_bench.py C4 > /dev/null 2>&1
+python scripts/launch_summary.py gpurun_out/eigl.csv > gpurun_out/eigl.txt 2>/dev/null; head -9 gpurun_out/eigl.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_random_shapes.py tests/test_gpu_full_size.py tests/test_gpu_c5.py tests/test_gpu_end_to_end.py -x -q 2>&1 | tail -1
+timeout 300 python scripts/random_sweep.py spectra 40 47 2>&1 | tail -1; timeout 300 python scripts/random_sweep.py core 12 53 --big 2>&1 | tail -1
