@@ -12,3 +12,5 @@ timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
 python scripts/launch_summary.py gpurun_out/r02y/scw_c4_launches.csv > gpurun_out/r02y/scw_c4_launches_summary.txt
 timeout 900 python bench.py --config C5 --steps 3 --warmup 2 --e2e-steps 0 --no-cpu-baseline > gpurun_out/r02y/bench_c5_1gpu.json 2> gpurun_out/r02y/bench_c5.err
 tail -c 300 gpurun_out/r02y/bench_c5_1gpu.json
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r02y/smoke.log 2>&1; tail -2 gpurun_out/r02y/smoke.log
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/r02y/pytest_gpu.log 2>&1; tail -2 gpurun_out/r02y/pytest_gpu.log
