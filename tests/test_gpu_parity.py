@@ -321,6 +321,23 @@ def test_scw_ragged_rows(m, n, k, r):
     _scw_parity(T, S, r)
 
 
+@pytest.mark.parametrize("m,n,k,r", [(65, 8, 19, 8), (96, 12, 30, 5)])
+def test_scw_sketch_wider_than_rows(m, n, k, r):
+    """n < k: rank(SA) <= n < k, so the pivoted-Cholesky basis stops at the rank (reading c2: the remaining
+    directions are dropped) -- errors against the oracle, and the rank-r factors of sketch_apply_scw give the
+    same reconstruction error as scw_error (r = n: exact up to the 3xTF32 floor)."""
+    g = torch.Generator().manual_seed(m + 1000 * n)
+    A = torch.rand(15, m, n, generator=g) - 0.3
+    T = torch.rand(4, m, n, generator=g) - 0.3
+    S, lam, info, st = tsk.sketch_train(A.cuda(), k)
+    err, eo = _scw_parity(T, S, r)
+    L, R, sg = tsk.sketch_apply_scw(T.cuda(), S, r)
+    ef = torch.linalg.norm((T.cuda().double() - torch.bmm(L.double(), R.double().transpose(1, 2))).reshape(4, -1),
+                           dim=1).cpu().numpy()
+    fro = np.linalg.norm(T.double().numpy().reshape(4, -1), axis=1)
+    assert np.all(np.abs(ef - err) <= SCW_TOL * err + 1e-6 * fro), (ef, err)
+
+
 def test_theorem1_holds_for_gpu_outputs():
     """P8 on the whole GPU path: GPU S, GPU SCW errors on the training set."""
     c = datagen.CONFIGS["C2"]
