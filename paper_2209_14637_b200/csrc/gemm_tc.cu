@@ -619,18 +619,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         {
           uint32_t hi[NC], lo[NC];
           if (a.xt) {
-            const float* xcol = reinterpret_cast<const float*>(raw_ptr(rs, 0)) + tt;
+            // explicit shared loads (a generic float* compiled to LD.E), all issued before the split
+            const uint32_t xcol = smem_u32(raw_ptr(rs, 0)) + (uint32_t)tt * 4u;
+            float e[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) e[c] = lds_f32(xcol + (uint32_t)((c0 + c) * kBM) * 4u);
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
-              const float e = xcol[(c0 + c) * kBM];
-              const uint32_t h = tf32_rn(e);
+              const uint32_t h = tf32_rn(e[c]);
               hi[c] = h;
-              lo[c] = __float_as_uint(e - __uint_as_float(h));
+              lo[c] = __float_as_uint(e[c] - __uint_as_float(h));
             }
             if (a.sq_part) {  // fp32 within the chunk (<= 32 positive terms), fp64 across chunks
               float cs = 0.f;
 #pragma unroll
-              for (int c = 0; c < NC; ++c) cs = fmaf(xcol[(c0 + c) * kBM], xcol[(c0 + c) * kBM], cs);
+              for (int c = 0; c < NC; ++c) cs = fmaf(e[c], e[c], cs);
               sq += (double)cs;
             }
           } else {
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // L_Y are written (row tt of the swizzled K-major tiles: 16-B chunk c at c ^ (tt & 7))
         if (kYT) {
           if (tt < a.bn) {
-            const float* ycol = reinterpret_cast<const float*>(raw_ptr(rs, diag ? 0 : 1)) + tt;
+            const uint32_t ycol = smem_u32(raw_ptr(rs, diag ? 0 : 1)) + (uint32_t)tt * 4u;
             const int ys = diag ? kBM : a.bn;  // row pitch (floats) of the raw tile
             const uint32_t hrow = smem_u32(lo_ptr(ls)) + (uint32_t)tt * 128u;
 #pragma unroll
@@ -677,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               float* lv = &l.x;
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                const float e = ycol[(c * 4 + j) * ys];
+                const float e = lds_f32(ycol + (uint32_t)((c * 4 + j) * ys) * 4u);
                 const float hh = __uint_as_float(__float_as_uint(e) & 0xFFFFE000u);
                 hv[j] = hh;
                 lv[j] = __uint_as_float(tf32_rn(e - hh));

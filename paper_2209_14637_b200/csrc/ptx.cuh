@@ -323,6 +323,11 @@ TSK_DEV void mma2_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+TSK_DEV float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 TSK_DEV float4 lds_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
