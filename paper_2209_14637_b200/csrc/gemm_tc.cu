@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 
 #include "ptx.cuh"
@@ -71,6 +72,9 @@ struct GemmArgs {
   int ldd;
   const int* only;   // batch mode: problems b with only[b] == 0 are skipped by every role (null: all)
   const int* only_any;  // optional device count of problems with only[b] != 0: 0 => the whole grid exits at once
+  int spin;  // TS kernel mbarrier waits without suspend hint: bit 0 TMA producer, 1 transform, 2 MMA issuer
+  unsigned long long* trace;  // diagnostics (TSK_TS_TRACE): per-chunk globaltimer stamps of CTA 0, [8][trace_n]
+  int trace_n;
   double* sq_part;   // TS kernel: [U][8] fp64 sums of the squared X elements of each unit (transform warps)
 };
 
@@ -79,6 +83,13 @@ struct GemmArgs {
 // batch has <= kOnlyMax problems (a CTA walks ~U / 148 units; one dependent global load per unit cost
 // ~65 us on a launch whose units were all skipped).
 constexpr int kOnlyMax = 256;  // 1 KB: the kYT variant has 225 KB of dynamic shared memory
+__device__ __forceinline__ void ts_wait(uint64_t* bar, uint32_t parity, bool spin) {
+  if (spin) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);
+}
+__device__ __forceinline__ void ts_stamp(const GemmArgs& a, int slot, long long i) {
+  if (a.trace && blockIdx.x == 0 && i < a.trace_n) a.trace[(size_t)slot * a.trace_n + i] = globaltimer_ns();
+}
 __device__ __forceinline__ bool unit_skipped(const GemmArgs& a, const int* s_only, int u) {
   if (a.only == nullptr) return false;
   const int b = (u % a.T) / a.T0;
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&rempty[i], 1);
     }
     for (int i = 0; i < kTsLoStages; ++i) {
-      mbar_init(&lfull[i], kSplitT ? 8 : 4);
+      mbar_init(&lfull[i], 4);  // the 4 transform warps of the group that converts the chunk
       mbar_init(&lempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -507,10 +518,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (; q < q1; q += 4, ci += 4) {
           const int sl = (int)(ci % RS);
           const uint32_t use = (uint32_t)((ci / RS) & 1);
-          mbar_wait(&rempty[sl], use ^ 1);
+          ts_wait(&rempty[sl], use ^ 1, a.spin & 1);
           const int z = (int)(q / a.cps);
           const int kc = (int)(q % a.cps) * kBK;
           if (isx) {
+            ts_stamp(a, 0, ci);
             mbar_arrive_expect_tx(&rfull[sl], (uint32_t)kTileBytes);
             if (a.xt) tma_load_3d(raw_ptr(sl, 0), &mapX, &rfull[sl], bi * kBM, kc, z);  // box {128 M, 32 K}
             else tma_load_3d(raw_ptr(sl, 0), &mapX, &rfull[sl], kc, bi * kBM, z);
@@ -549,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t rph = 0, lph = 0;
       int ab = 0;
       uint32_t aph = 0;
+      long long tci = 0;  // CTA-wide chunk index (trace)
       for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
         if (unit_skipped(a, s_only, u)) continue;
         int t, bi, bj;
@@ -559,11 +572,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         int cpos = 0;
         for (long long q = q0; q < q1; ++q) {
           if (cpos == 0) {
-            mbar_wait(&acce[ab], aph ^ 1);
+            ts_wait(&acce[ab], aph ^ 1, a.spin & 4);
             tc_fence_after();
           }
-          mbar_wait(&lfull[ls], lph);  // transform done: implies the raw stage landed
+          ts_wait(&lfull[ls], lph, a.spin & 4);  // transform done: implies the raw stage landed
           tc_fence_after();
+          ts_stamp(a, 1, tci);
           // bn = 128: one accumulator per buffer; bn = 64: separate H H^T and cross accumulators
           // (the truncating accumulation error then comes from the H H^T chain only)
           const uint32_t d = tmem_base + (uint32_t)ab * kTsAccCols;
@@ -584,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&rempty[rs]);
           if (++rs == RS) { rs = 0; rph ^= 1; }
           mma_commit(&lempty[ls]);
+          ts_stamp(a, 2, tci++);
           if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
           if (++cpos == a.chain || q + 1 == q1) {
             mma_commit(&accf[ab]);
@@ -597,11 +612,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== transform: X rows -> TMEM (H, L); Y tile -> L_Y in shared memory ========
     const int quad = warp & 3;         // the TMEM lane quadrant of this warp
     const int tt = quad * 32 + lane;   // 0..127 = tile row handled for the TMEM A operand
-    constexpr int NC = kSplitT ? 16 : 32;  // K-columns of the chunk converted by this warp
+    // kSplitT (N = 64): two groups of 4 warps (4-7, 12-15) convert alternate chunks, all 32 K-columns each,
+    // so two chunks' conversions overlap (the per-chunk chain load -> split -> tcgen05.st -> wait -> fence ->
+    // arrive was ~420 ns of latency with both groups on the same chunk, 16 columns each; scripts/ts_trace.py)
+    constexpr int NC = 32;
     const int grp = (kSplitT && warp >= 12) ? 1 : 0;
-    const int c0 = grp * NC;
+    constexpr int c0 = 0;
     int rs = 0, ls = 0;
     uint32_t rph = 0, lph = 0;
+    long long tfi = 0;  // CTA-wide chunk index (trace)
     for (int u = blockIdx.x; u < a.U; u += gridDim.x) {
       if (unit_skipped(a, s_only, u)) continue;
       int t, bi, bj;
@@ -611,8 +630,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool diag = a.sym && bi == bj;
       double sq = 0.0;  // this thread's sum of squared X elements over the unit (a.sq_part)
       for (long long q = q0; q < q1; ++q) {
-        mbar_wait(&rfull[rs], rph);
-        mbar_wait(&lempty[ls], lph ^ 1);
+        if (kSplitT && (int)(tfi & 1) != grp) {  // the other group's chunk: advance the rings only
+          ++tfi;
+          if (++rs == RS) { rs = 0; rph ^= 1; }
+          if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
+          continue;
+        }
+        ts_wait(&rfull[rs], rph, a.spin & 2);
+        if (tt == 0) ts_stamp(a, 3, tfi);
+        ts_wait(&lempty[ls], lph ^ 1, a.spin & 2);
+        if (tt == 0) ts_stamp(a, 4, tfi);
         tc_fence_after();
         // (1) row tt of X (128-B swizzled row: 16-B chunk c at position c ^ (tt & 7)); for a
         // transposed X the raw tile is [32 K][128 M] unswizzled and row tt of X is column tt
@@ -694,8 +721,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t src = smem_u32(raw_ptr(rs, diag ? 0 : 1));
           const uint32_t dst = smem_u32(lo_ptr(ls));
           const int nyv = a.bn * (kBK * 4 / 16);  // float4 of the bn used rows
-          constexpr int kTT = kSplitT ? 256 : 128;  // transform threads
-          for (int i = grp * 128 + tt; i < nyv; i += kTT) {
+          constexpr int kTT = 128;  // transform threads of the group
+          for (int i = tt; i < nyv; i += kTT) {
             const uint32_t off = (uint32_t)i * 16u;
             const float4 v = lds_f4(src + off);
             float4 l;
@@ -718,6 +745,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&lfull[ls]);
+        if (tt == 0) ts_stamp(a, 5, tfi);
+        ++tfi;
         if (++rs == RS) { rs = 0; rph ^= 1; }
         if (++ls == kTsLoStages) { ls = 0; lph ^= 1; }
       }
@@ -1107,6 +1136,15 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   a.res_part = p.res_part;
   a.only = p.only;
   a.only_any = p.only_any;
+  a.spin = getenv("TSK_TS_SPIN") ? atoi(getenv("TSK_TS_SPIN")) : 0;
+  a.trace = nullptr;
+  a.trace_n = 0;
+  const char* ts_trace = getenv("TSK_TS_TRACE");  // diagnostics: scripts/ts_trace.py
+  if (ts_trace) {
+    a.trace_n = 8192;
+    if (cudaMalloc(&a.trace, (size_t)8 * a.trace_n * 8) != cudaSuccess) return TSK_ENOMEM;
+    cudaMemsetAsync(a.trace, 0, (size_t)8 * a.trace_n * 8, ctx->stream);
+  }
   a.sq_part = p.sq_part;
   if ((p.only || p.sq_part) && !p.batch) return TSK_EINVAL;
   a.dout = p.dout;
@@ -1164,6 +1202,16 @@ tsk_status gemm_tf32x3(Ctx* ctx, const GemmProblem& p) {
   }
   if (launch_status("gemm_tf32x3") != TSK_OK) return TSK_ECUDA;
   ctx->count_launch();
+  if (ts_trace) {
+    std::vector<unsigned long long> h((size_t)8 * a.trace_n);
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    cudaFree(a.trace);
+    if (FILE* f = fopen(ts_trace, "ab")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   if (a.dout || a.resA) {
     if (p.info) {
       p.info->splits = a.S;
