@@ -1120,9 +1120,19 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     int d = 1;
     if (b > a && xmax > 1.0 + 1e-12) {
       // T_d(x) ~ exp(d acosh x) / 2 <= R: R = 1e4 on the random first block (its columns carry O(1)
-      // components along the top eigenvectors), 1e7 once the block holds Ritz vectors
+      // components along the top eigenvectors), 1e7 once the block holds Ritz vectors.
+      // Steep top (x_max >= 4: the degree is bounded by the largest active eigenvalue, not by the
+      // cap): the range is the amplification of the TOP directions against the block edge, and after
+      // a Rayleigh-Ritz step a Ritz column carries a top eigenvector only through that vector's angle
+      // to the block, which the earlier filters shrank fastest -- 1e13 keeps the column-scaled block
+      // Gram well conditioned there (C3/C4: 7 -> 5 Rayleigh-Ritz steps; the CholQR fallbacks stay
+      // armed).  Flat tops keep 1e7: there the degree is set by the cap and a larger range only
+      // overshoots the last filter (C5: 59 -> 73 products at 1e9; reading c15).
       static const double range = getenv("TSK_EIG_RANGE") ? atof(getenv("TSK_EIG_RANGE")) : 1e7;
-      const double R = (outer == 0 ? 1e4 : range) * range_cut;
+      static const double steep = getenv("TSK_EIG_STEEP_MAX") ? atof(getenv("TSK_EIG_STEEP_MAX")) : 1e13;
+      double R = outer == 0 ? 1e4 : range;
+      if (outer > 0 && xmax >= 4.0) R = std::max(R, steep);
+      R *= range_cut;
       d = (int)std::floor(std::log(2.0 * std::max(R, 10.0)) / std::acosh(xmax));
       d = std::max(1, std::min(d, opt.cheb_degree > 0 ? opt.cheb_degree : 40));
     }
