@@ -1077,9 +1077,14 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
       break;
     }
     if (outer + 1 == max_iters) break;
-    // ---- lock the leading converged pairs well above the wanted edge
+    // ---- lock the leading converged pairs well above the wanted edge.  Deflating a pair whose residual is
+    // res perturbs G' by ~res (absolute), so besides res <= 1e-8 theta_i the residual must sit below the
+    // accuracy still asked of the wanted edge (0.1 tol theta_k): with a steep top over a flat bulk (top / edge
+    // ~ 1e3 and more) the relative rule alone left a ~1e-5 floor in G' and the bulk stagnated at the
+    // iteration cap (tests/test_gpu_random_shapes.py, steep)
     int nnew = 0;
-    while (nnew < kr - 1 && hres[nnew] <= 1e-8 * hth[nnew] && hth[nnew] >= 2.0 * thk) ++nnew;
+    while (nnew < kr - 1 && hres[nnew] <= std::min(1e-8 * hth[nnew], 0.1 * tol * thk) && hth[nnew] >= 2.0 * thk)
+      ++nnew;
     if (nnew > 0) {
       copy_cols_kernel<<<nblk((long long)m * nnew, 256), 256, 0, s>>>(X, pa, 0, Xl, p, nl, m, nnew);
       cudaMemcpyAsync(thl + nl, theta, (size_t)nnew * 8, cudaMemcpyDeviceToDevice, s);

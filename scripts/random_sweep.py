@@ -162,7 +162,7 @@ def suite_mixed(ncase, rng):
 
 def suite_spectra(ncase, rng):
     bad = 0
-    kinds = ["flat", "geometric", "clustered", "rankdef", "dominant", "twogap"]
+    kinds = ["flat", "geometric", "clustered", "rankdef", "dominant", "twogap", "steep"]
     for t in range(ncase):
         m = int(rng.integers(257, 1500)); k = int(rng.integers(1, 101))
         kind = kinds[t % len(kinds)]
@@ -176,6 +176,9 @@ def suite_spectra(ncase, rng):
             rk = int(rng.integers(1, 2 * k + 2)); lam = np.zeros(m); lam[:rk] = rng.random(rk) + 0.1
         elif kind == "dominant":
             lam = 1.0 + rng.random(m); lam[0] = 1e5
+        elif kind == "steep":  # dominant mean, power-law top over a nearly flat bulk (C4-like, exaggerated)
+            lam = 1.0 + 0.05 * rng.random(m); nt = int(rng.integers(2, 30))
+            lam[1:nt + 1] += float(10 ** rng.uniform(2, 5)) * np.arange(1, nt + 1) ** -1.5; lam[0] = 1e6
         else:
             lam = np.concatenate([np.full(k, 10.0), np.full(m - k, 1.0)]) + 1e-3 * rng.random(m)
         U, _ = torch.linalg.qr(torch.randn(m, m, dtype=torch.float64, device="cuda"))
