@@ -886,6 +886,10 @@ tsk_status topk_eigen_ex(Ctx* ctx, const double* G64, int m, int k, float* S, do
     // residual is ~ ratio * r1 when the convergence is geometric
     const double ratio = r0 > 0.0 ? r1 / r0 : 0.0;
     if (trace) fprintf(stderr, "[eig] power: theta %.10e res/theta %.2e ratio %.2e\n", th, r1 / th, ratio);
+    // (its residual can exceed 0.1 tol theta_k, unlike the block iteration's locking rule below, but the
+    // error of a power iterate lies along the next TOP eigenvectors -- bulk components fell by
+    // (lambda_bulk / theta_1)^6 -- so the deflation perturbs G' only inside the top subspace:
+    // test_eigensolver_spectra[dominant2])
     if (th > 0.0 && ratio <= 0.05 && r1 * ratio <= 1e-10 * th && k > 1) {
       copy_cols_kernel<<<nblk(m, 256), 256, 0, s>>>(v, 1, 0, Xl, p, 0, m, 1);
       cudaMemcpyAsync(thl, pw + 2 * (kPower - 1), 8, cudaMemcpyDeviceToDevice, s);

@@ -66,17 +66,21 @@ def test_random_two_sided_and_matrix_free(seed):
         assert np.max(np.abs(lamm.cpu().numpy() - th[:kk])) <= 1e-5 * th[0]
 
 
-@pytest.mark.parametrize("kind", ["dominant", "clustered", "rankdef", "steep"])
+@pytest.mark.parametrize("kind", ["dominant", "clustered", "rankdef", "steep", "dominant2"])
 def test_eigensolver_spectra(kind):
     """Synthetic spectra for the subspace-iteration eigensolver (m > 256): a dominant eigenvalue above a
     flat rest (the case the residual-only stopping rule under-converged), clusters, rank deficiency, and a
     steep power-law top over a nearly flat bulk below a dominant mean (the C4 shape, exaggerated: the
     filter runs at the 1e13 steep-spectrum range)."""
-    rng = np.random.default_rng({"dominant": 1, "clustered": 2, "rankdef": 3, "steep": 4}[kind])
+    rng = np.random.default_rng({"dominant": 1, "clustered": 2, "rankdef": 3, "steep": 4, "dominant2": 5}[kind])
     m, k = 700, 40
     if kind == "dominant":
         lam = 1.0 + rng.random(m)
         lam[0] = 1e5
+    elif kind == "dominant2":  # a dominant pair only 50x above the next, locked by the power pre-pass with a
+        lam = 1.0 + 0.05 * rng.random(m)  # residual above 0.1 tol theta_k (its error lies along the top pair)
+        lam[1] = 2e4
+        lam[0] = 1e6
     elif kind == "steep":
         lam = 1.0 + 0.05 * rng.random(m)
         lam[1:13] += 2000.0 * np.arange(1, 13) ** -1.5
@@ -94,7 +98,7 @@ def test_eigensolver_spectra(kind):
     w = np.sort(lam)[::-1]
     assert (w[:k].sum() - tucker1.kyfan_energy(G, Sd)) <= 1e-6 * w[:k].sum()
     assert np.linalg.norm(Sd @ Sd.T - np.eye(k)) <= 1e-5
-    if kind == "steep":
+    if kind in ("steep", "dominant2"):
         # converged without a fallback status; Ritz values below their eigenvalues (interlacing) and within
         # the Ky Fan stopping deficit of them (reading c15); the bulk gap at k is ~1.0 -- no projector claim
         assert st == 0, info.as_dict()
