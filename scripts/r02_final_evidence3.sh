@@ -1,5 +1,4 @@
-# Round-2 closing evidence after the eigensolver range change (1 x B200): bench line, launch lists of the step / eigensolver / SCW, C5 bench line, smoke, GPU tests, random sweeps.  Outputs under gpurun_out/r02z/.
-# the step / eigensolver / SCW, C5 bench line.  Outputs under gpurun_out/r02z/.
+# Round-2 closing evidence (1 x B200): bench line, launch lists of the step / eigensolver / SCW, C5 bench line, smoke, GPU tests, random sweeps.  Outputs under gpurun_out/r02z/.
 set -x
 mkdir -p gpurun_out/r02z
 timeout 600 python bench.py > gpurun_out/r02z/bench_1gpu.json 2> gpurun_out/r02z/bench_1gpu.err
