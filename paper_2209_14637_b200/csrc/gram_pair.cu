@@ -733,7 +733,7 @@ tsk_status gram_pair(Ctx* ctx, const GemmProblem& p) {
   a.lag = p.lag >= 0 ? (p.lag + kZ - 1) / kZ : 64 / kZ;
   // developer overrides (scripts/gram_pair_time.py sweeps)
   if (const char* ev = getenv("TSK_PAIR_FOLD")) a.fold = std::max(1, atoi(ev));
-  if (const char* ev = getenv("TSK_PAIR_LAG")) a.lag = std::max(1, (atoi(ev) + kZ - 1) / kZ);
+  if (const char* ev = getenv("TSK_PAIR_LAG")) a.lag = atoi(ev) <= 0 ? 0 : std::max(1, (atoi(ev) + kZ - 1) / kZ);  // 0: throttle off
   a.part = part;
   a.progress = prog;
   // diagnostics only (developer experiments, scripts/gram_pair_*.py): TSK_PAIR_DIAG bit 0 = skip
